@@ -1,0 +1,241 @@
+/*
+ * nnl.h — C ABI of libnnl.so, the B200 (sm_100a) hot path behind the
+ * nanonnl operator API (reference: /root/reference/pkg/src/nanonnl).
+ *
+ * Conventions:
+ *   - every entry point returns int32 status; 0 = OK, nonzero codes map 1:1
+ *     onto the reference exception classes (src/errors.py:8-122);
+ *     nnl_last_error() returns a thread-local message for the last failure;
+ *   - all tensors are caller-owned DEVICE pointers; 4-D activations are
+ *     NHWC (channels innermost), conv weights are KRSC ([out][kh][kw][in]),
+ *     affine weights keep the reference (I,O) row-major layout;
+ *   - dtype codes: NNL_F32 = 0, NNL_F16 = 1 (binary16 storage, fp32 math);
+ *   - every call is asynchronous on the cudaStream_t passed as `stream`
+ *     (void* here so the header needs no CUDA includes);
+ *   - `accumulate` flags implement the reference's NdArray.accumulate
+ *     (src/tensor.py:115-123): out = q(out + result) instead of q(result);
+ *   - `nonfinite` pointers (nullable) receive an OR of "some written value
+ *     is inf/NaN" (src/tensor.py:153-157) so the solver needs no extra pass.
+ *
+ * Each function names the reference interface it replaces.
+ */
+#ifndef NNL_H_
+#define NNL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (src/errors.py) ------------------------------------- */
+#define NNL_OK 0
+#define NNL_ERR_SHAPE_MISMATCH 1          /* errors.py:14  ShapeMismatch */
+#define NNL_ERR_KERNEL_TOO_LARGE 2        /* errors.py:22  KernelTooLarge */
+#define NNL_ERR_LABEL_OUT_OF_RANGE 3      /* errors.py:44  LabelOutOfRange */
+#define NNL_ERR_DEGENERATE_BATCH 4        /* errors.py:48  DegenerateBatch */
+#define NNL_ERR_NOT_SETUP 5               /* errors.py:64  NotSetup */
+#define NNL_ERR_COLLECTIVE_TIMEOUT 6      /* errors.py:78  CollectiveTimeout */
+#define NNL_ERR_SHAPE_MISMATCH_RANKS 7    /* errors.py:74  ShapeMismatchAcrossRanks */
+#define NNL_ERR_INVALID_RANGE 8           /* errors.py:18  InvalidRange */
+#define NNL_ERR_CUDA 20                   /* CUDA runtime/driver failure */
+#define NNL_ERR_UNSUPPORTED 21            /* configuration not implemented */
+#define NNL_ERR_INVALID_ARGUMENT 22
+
+#define NNL_F32 0
+#define NNL_F16 1
+
+const char* nnl_last_error(void);
+int nnl_version(void);
+/* number of kernels this library launched since load (or since reset) */
+int64_t nnl_launch_count(int reset);
+/* 1 when the tensor-core (tcgen05) path is enabled for eligible shapes */
+int nnl_set_tc_enabled(int enabled);
+
+/* ---- geometry ----------------------------------------------------------- */
+typedef struct nnl_conv_shape {
+  int32_t n, h, w, c;          /* input, NHWC */
+  int32_t k;                   /* output maps */
+  int32_t r, s;                /* kernel (kh, kw) */
+  int32_t stride_h, stride_w;
+  int32_t pad_h, pad_w;
+  int32_t p, q;                /* output extent; functions.py:122-125 */
+} nnl_conv_shape;
+
+typedef struct nnl_pool_shape {
+  int32_t n, h, w, c;          /* input, NHWC */
+  int32_t kh, kw, sh, sw, ph, pw;
+  int32_t p, q;                /* output extent (ignore_border already applied) */
+} nnl_pool_shape;
+
+/* ---- storage / numerics: src/tensor.py ---------------------------------- */
+/* tensor.py:46-59 quantize_f16 applied to an f32 buffer (RNE, overflow->inf) */
+int nnl_quantize_f16(int64_t n, const float* x, float* y, void* stream);
+/* NdArray.fill (tensor.py:125-131); value is quantized for F16 */
+int nnl_fill(int dtype, int64_t n, void* dst, float value, void* stream);
+/* fill from a device scalar (double), used for the dynamic loss-scale seed */
+int nnl_fill_from_device(int dtype, int64_t n, void* dst, const double* value, void* stream);
+/* NdArray.accumulate / write of another device buffer of the same dtype */
+int nnl_accumulate(int dtype, int64_t n, const void* src, void* dst, int accumulate, void* stream);
+/* has_inf_or_nan over one buffer (tensor.py:153-157); ORs into *flag */
+int nnl_nonfinite(int dtype, int64_t n, const void* x, int32_t* flag, void* stream);
+/* RngState.next_uniform (tensor.py:241-252): draw i = f(seed, counter+i) */
+int nnl_rng_uniform(uint64_t seed, uint64_t counter, int64_t n, double low, double high,
+                    int dtype, void* out, void* stream);
+
+/* ---- Affine: functions.py:82-119 ---------------------------------------- */
+/* pass: 0 forward, 1 backward-data, 2 backward-weight.  in_c: channel count of an
+   NHWC input (weight rows follow its logical NCHW flattening); in_f for 2-D x */
+size_t nnl_affine_workspace_size(int dtype, int64_t batch, int64_t in_f, int64_t out_f, int pass);
+int nnl_affine_fwd(int dtype, int64_t batch, int64_t in_f, int64_t in_c, int64_t out_f,
+                   const void* x, const void* w, const void* b, void* y,
+                   void* ws, size_t ws_bytes, void* stream);
+int nnl_affine_bwd_data(int dtype, int64_t batch, int64_t in_f, int64_t in_c, int64_t out_f,
+                        const void* dy, const void* w, void* dx, int accumulate,
+                        void* ws, size_t ws_bytes, void* stream);
+int nnl_affine_bwd_weight(int dtype, int64_t batch, int64_t in_f, int64_t in_c, int64_t out_f,
+                          const void* x, const void* dy, void* dw, int acc_w,
+                          void* db, int acc_b, int32_t* nonfinite,
+                          void* ws, size_t ws_bytes, void* stream);
+
+/* ---- Convolution: functions.py:152-214 ---------------------------------- */
+size_t nnl_conv2d_workspace_size(const nnl_conv_shape* cs, int dtype, int pass);
+/* y = conv(x, w) + b.  stat_partials (nullable, f32 [ceil(M/128)][2][K]) receives
+   per-row-tile sum / sum of squares of the ROUNDED outputs for a following BN. */
+int nnl_conv2d_fwd(const nnl_conv_shape* cs, int dtype, const void* x, const void* w,
+                   const void* b, void* y, float* stat_partials,
+                   void* ws, size_t ws_bytes, void* stream);
+int nnl_conv2d_bwd_data(const nnl_conv_shape* cs, int dtype, const void* dy, const void* w,
+                        void* dx, int accumulate, void* ws, size_t ws_bytes, void* stream);
+int nnl_conv2d_bwd_weight(const nnl_conv_shape* cs, int dtype, const void* x, const void* dy,
+                          void* dw, int acc_w, void* db, int acc_b, int32_t* nonfinite,
+                          void* ws, size_t ws_bytes, void* stream);
+/* number of stat-partial rows nnl_conv2d_fwd writes (0 if fusion unsupported) */
+int32_t nnl_conv2d_stat_rows(const nnl_conv_shape* cs, int dtype);
+
+/* ---- MaxPooling: functions.py:217-291 ----------------------------------- */
+int nnl_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x, void* y,
+                    uint8_t* argmax, void* stream);
+int nnl_maxpool_bwd(int dtype, const nnl_pool_shape* ps, const void* dy,
+                    const uint8_t* argmax, void* dx, int accumulate, void* stream);
+
+/* ---- ReLU: functions.py:294-317 ----------------------------------------- */
+int nnl_relu_fwd(int dtype, int64_t n, const void* x, void* y, void* stream);
+/* gx = gy * (x > 0) as a multiply (inf*0 = NaN); `x` may be the ReLU output */
+int nnl_relu_bwd(int dtype, int64_t n, const void* x, const void* dy, void* dx,
+                 int accumulate, void* stream);
+
+/* ---- Add2 / GlobalAveragePooling (extensions, oracle/nnl_oracle.py) ----- */
+int nnl_add2_fwd(int dtype, int64_t n, const void* a, const void* b, void* y,
+                 int fuse_relu, void* stream);
+int nnl_gap_fwd(int dtype, int64_t n, int64_t hw, int64_t c, const void* x, void* y,
+                void* stream);
+int nnl_gap_bwd(int dtype, int64_t n, int64_t hw, int64_t c, const void* dy, void* dx,
+                int accumulate, void* stream);
+
+/* ---- SoftmaxCrossEntropy: functions.py:320-360 -------------------------- */
+/* labels are stored in `dtype`; loss_out is a rank-0 buffer of `dtype`;
+   row_stats (f32 [3*batch]) keeps (max, logsumexp, log p[label]) per row;
+   label_err (nullable) is set to 1 on a label outside [0,classes) */
+int nnl_sce_fwd(int dtype, int64_t batch, int64_t classes, const void* logits,
+                const void* labels, void* loss_out, float* row_stats,
+                int32_t* label_err, void* stream);
+int nnl_sce_bwd(int dtype, int64_t batch, int64_t classes, const void* logits,
+                const void* labels, const float* row_stats, const void* gloss,
+                void* glogits, int accumulate, void* stream);
+
+/* ---- BatchNormalization: functions.py:363-441 --------------------------- */
+size_t nnl_bn_workspace_size(int64_t rows, int32_t c);
+/* rows = N*H*W (channel-innermost).  stat_partials (nullable) are the conv
+   epilogue partials; save_mean/save_istd (f32 [c]) feed backward. */
+int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x,
+                     const float* gamma, const float* beta,
+                     float* running_mean, float* running_var, float eps, float momentum,
+                     const float* stat_partials, int32_t n_partials,
+                     float* save_mean, float* save_istd, void* y, int fuse_relu,
+                     void* ws, size_t ws_bytes, void* stream);
+int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x,
+                    const float* gamma, const float* beta, const float* mean,
+                    const float* var, float eps, float* save_mean, float* save_istd,
+                    void* y, int fuse_relu, void* stream);
+/* relu_out (nullable): gate gy by (relu_out > 0) first (fused BN->ReLU) */
+int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy,
+               const void* relu_out, const float* gamma, const float* save_mean,
+               const float* save_istd, int batch_stat,
+               void* dx, int acc_x, float* dgamma, int acc_g, float* dbeta, int acc_b,
+               int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- Solver: solver.py:67-164 ------------------------------------------- */
+typedef struct nnl_param_slot {
+  void* data;        /* visible weight (dtype) */
+  void* grad;        /* gradient (dtype) */
+  float* master;     /* f32 master (solver.py:89-92) */
+  float* momentum;   /* f32 velocity (extension; nullable) */
+  int64_t n;
+  int32_t dtype;
+  int32_t pad_;
+} nnl_param_slot;
+
+/* multi-tensor work list: chunk i covers slot[slot] elements [start, start+len) */
+typedef struct nnl_chunk {
+  int32_t slot;
+  int32_t len;
+  int64_t start;
+} nnl_chunk;
+
+/* device-resident DynamicLossScaler (solver.py:49-64) + step outcome */
+typedef struct nnl_scaler_state {
+  double loss_scale;
+  double scaling_factor;
+  int64_t interval;
+  int64_t counter;
+  int32_t nonfinite;   /* OR of the current step's grads (reset by nnl_scaler_finish) */
+  int32_t applied;     /* outcome of the last step: 1 Applied, 0 SkippedInfNan */
+} nnl_scaler_state;
+
+/* has_inf_or_nan over every slot grad (solver.py:115-117); ORs into *flag */
+int nnl_multi_nonfinite(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                        int32_t* flag, void* stream);
+/* scale_grad (solver.py:106-109): g <- q(g * f32(factor)) */
+int nnl_multi_scale_grad(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                         float factor, void* stream);
+/* sum of squares of every grad in f64 (clip_grad_by_norm, solver.py:119-129) */
+int nnl_multi_sumsq(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                    double* out, void* stream);
+/* one fused HBM pass (solver.py:100-109,132-155):
+ *   scaler == NULL: plain update; else skip when scaler->nonfinite, otherwise
+ *   unscale g <- q(g*f32(1/S)) first.
+ *   update: d = g + wd*master; v = momentum*v + lr*d; master -= v; w = q(master)
+ *   which with momentum = wd = 0 is exactly  master -= f32(lr)*g  (reference).
+ *   momentum/weight_decay are the unpinned extension (NNabla Momentum/weight decay). */
+int nnl_multi_sgd_update(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                         float lr, float momentum, float weight_decay,
+                         nnl_scaler_state* scaler, void* stream);
+/* scaler bookkeeping after the update (dynamic_step tail, solver.py:142-153) */
+int nnl_scaler_finish(nnl_scaler_state* scaler, void* stream);
+
+/* ---- Data-parallel all_reduce: communicator.py:69-105 ------------------- */
+/* slots[i].data is unused here; bucket element = slot offset given by the
+ * chunk table's running position: chunk i lands at bucket[chunk_pos[i]]   */
+int nnl_bucket_pack(const nnl_param_slot* slots, const nnl_chunk* chunks, const int64_t* chunk_pos,
+                    int32_t n_chunks, float* bucket, void* stream);
+/* grad = q(bucket / f32(world)); ORs non-finite results into *nonfinite */
+int nnl_bucket_unpack_mean(const nnl_param_slot* slots, const nnl_chunk* chunks,
+                           const int64_t* chunk_pos, int32_t n_chunks, const float* bucket,
+                           int32_t world, int32_t* nonfinite, void* stream);
+
+/* ---- API-boundary marshaling (Variable.d get/set, graph.py:137-155) ------
+ * import: f32 NCHW (logical, host order) -> dtype NHWC storage, quantizing;
+ * export: dtype NHWC storage -> f32 NCHW.  Non-4-D buffers use n=c=1. */
+int nnl_import_f32(int dtype, int32_t n, int32_t c, int32_t hw, const float* src, void* dst,
+                   void* stream);
+int nnl_export_f32(int dtype, int32_t n, int32_t c, int32_t hw, const void* src, float* dst,
+                   void* stream);
+/* in-process rank-ordered fold (communicator.py:99-103): out = b0 + b1 + ... (f32) */
+int nnl_fold_f32(int32_t k, const float* const* bufs_dev, int64_t n, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNL_H_ */

@@ -1,0 +1,202 @@
+"""ctypes binding of libnnl.so (include/nnl.h) and device plumbing.
+
+This is the only module that talks to the native library.  Every call goes
+through :func:`call`, which turns a nonzero status into the matching
+exception class of :mod:`errors`.  There is no fallback: if the shared
+library is missing, or no CUDA device is visible, using the package raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import errors as E
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnnl.so")
+
+F32, F16 = 0, 1
+
+_STATUS = {
+    1: E.ShapeMismatch,
+    2: E.KernelTooLarge,
+    3: E.LabelOutOfRange,
+    4: E.DegenerateBatch,
+    5: E.NotSetup,
+    6: E.CollectiveTimeout,
+    7: E.ShapeMismatchAcrossRanks,
+    8: E.InvalidRange,
+}
+
+p = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+u64 = C.c_uint64
+f32 = C.c_float
+f64 = C.c_double
+sz = C.c_size_t
+
+
+class ConvShape(C.Structure):
+    _fields_ = [(n, i32) for n in ("n", "h", "w", "c", "k", "r", "s", "stride_h", "stride_w",
+                                   "pad_h", "pad_w", "p", "q")]
+
+
+class PoolShape(C.Structure):
+    _fields_ = [(n, i32) for n in ("n", "h", "w", "c", "kh", "kw", "sh", "sw", "ph", "pw",
+                                   "p", "q")]
+
+
+class ParamSlot(C.Structure):
+    _fields_ = [("data", p), ("grad", p), ("master", p), ("momentum", p), ("n", i64),
+                ("dtype", i32), ("pad_", i32)]
+
+
+class Chunk(C.Structure):
+    _fields_ = [("slot", i32), ("len", i32), ("start", i64)]
+
+
+class ScalerState(C.Structure):
+    _fields_ = [("loss_scale", f64), ("scaling_factor", f64), ("interval", i64),
+                ("counter", i64), ("nonfinite", i32), ("applied", i32)]
+
+
+_SIGS = {
+    "nnl_last_error": (C.c_char_p, []),
+    "nnl_version": (C.c_int, []),
+    "nnl_launch_count": (i64, [C.c_int]),
+    "nnl_set_tc_enabled": (C.c_int, [C.c_int]),
+    "nnl_quantize_f16": (C.c_int, [i64, p, p, p]),
+    "nnl_fill": (C.c_int, [C.c_int, i64, p, f32, p]),
+    "nnl_fill_from_device": (C.c_int, [C.c_int, i64, p, p, p]),
+    "nnl_accumulate": (C.c_int, [C.c_int, i64, p, p, C.c_int, p]),
+    "nnl_nonfinite": (C.c_int, [C.c_int, i64, p, p, p]),
+    "nnl_rng_uniform": (C.c_int, [u64, u64, i64, f64, f64, C.c_int, p, p]),
+    "nnl_affine_workspace_size": (sz, [C.c_int, i64, i64, i64, C.c_int]),
+    "nnl_affine_fwd": (C.c_int, [C.c_int, i64, i64, i64, i64, p, p, p, p, p, sz, p]),
+    "nnl_affine_bwd_data": (C.c_int, [C.c_int, i64, i64, i64, i64, p, p, p, C.c_int, p, sz, p]),
+    "nnl_affine_bwd_weight": (C.c_int, [C.c_int, i64, i64, i64, i64, p, p, p, C.c_int, p,
+                                        C.c_int, p, p, sz, p]),
+    "nnl_conv2d_workspace_size": (sz, [p, C.c_int, C.c_int]),
+    "nnl_conv2d_stat_rows": (i32, [p, C.c_int]),
+    "nnl_conv2d_fwd": (C.c_int, [p, C.c_int, p, p, p, p, p, p, sz, p]),
+    "nnl_conv2d_bwd_data": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, sz, p]),
+    "nnl_conv2d_bwd_weight": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, C.c_int, p, p, sz, p]),
+    "nnl_maxpool_fwd": (C.c_int, [C.c_int, p, p, p, p, p]),
+    "nnl_maxpool_bwd": (C.c_int, [C.c_int, p, p, p, p, C.c_int, p]),
+    "nnl_relu_fwd": (C.c_int, [C.c_int, i64, p, p, p]),
+    "nnl_relu_bwd": (C.c_int, [C.c_int, i64, p, p, p, C.c_int, p]),
+    "nnl_add2_fwd": (C.c_int, [C.c_int, i64, p, p, p, C.c_int, p]),
+    "nnl_gap_fwd": (C.c_int, [C.c_int, i64, i64, i64, p, p, p]),
+    "nnl_gap_bwd": (C.c_int, [C.c_int, i64, i64, i64, p, p, C.c_int, p]),
+    "nnl_sce_fwd": (C.c_int, [C.c_int, i64, i64, p, p, p, p, p, p]),
+    "nnl_sce_bwd": (C.c_int, [C.c_int, i64, i64, p, p, p, p, p, C.c_int, p]),
+    "nnl_bn_workspace_size": (sz, [i64, i32]),
+    "nnl_bn_fwd_train": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, f32, f32, p, i32, p, p, p,
+                                   C.c_int, p, sz, p]),
+    "nnl_bn_fwd_eval": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, f32, p, p, p, C.c_int, p]),
+    "nnl_bn_bwd": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, p, C.c_int, p, C.c_int, p,
+                             C.c_int, p, C.c_int, p, p, sz, p]),
+    "nnl_multi_nonfinite": (C.c_int, [p, p, i32, p, p]),
+    "nnl_multi_scale_grad": (C.c_int, [p, p, i32, f32, p]),
+    "nnl_multi_sumsq": (C.c_int, [p, p, i32, p, p]),
+    "nnl_multi_sgd_update": (C.c_int, [p, p, i32, f32, f32, f32, p, p]),
+    "nnl_scaler_finish": (C.c_int, [p, p]),
+    "nnl_bucket_pack": (C.c_int, [p, p, p, i32, p, p]),
+    "nnl_bucket_unpack_mean": (C.c_int, [p, p, p, i32, p, i32, p, p]),
+    "nnl_fold_f32": (C.c_int, [i32, p, i64, p, p]),
+    "nnl_import_f32": (C.c_int, [C.c_int, i32, i32, i32, p, p, p]),
+    "nnl_export_f32": (C.c_int, [C.c_int, i32, i32, i32, p, p, p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libnnl.so once; raise DeviceError if it is absent (no fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise E.DeviceError(
+                        f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                        "(make -C paper_2102_06725_b200/csrc)")
+                handle = C.CDLL(LIB_PATH)
+                for name, (res, args) in _SIGS.items():
+                    fn = getattr(handle, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)
+
+
+def last_error() -> str:
+    return lib().nnl_last_error().decode(errors="replace")
+
+
+def call(name: str, *args) -> int:
+    """Invoke a status-returning entry point; raise the mapped error class."""
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = last_error()
+        raise _STATUS.get(rc, E.DeviceError)(f"{name}: {msg} (status {rc})")
+    return rc
+
+
+# --- device plumbing ----------------------------------------------------------
+
+_torch = None
+
+
+def torch():
+    """PyTorch is used for device memory, streams and torch.distributed only."""
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise E.DeviceError("no CUDA device visible: this package has no CPU path")
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream() -> int:
+    """Raw cudaStream_t of torch's current stream on the current device."""
+    return torch().cuda.current_stream().cuda_stream
+
+
+class _Workspace(threading.local):
+    def __init__(self):
+        self.buf = None
+
+
+_ws = _Workspace()
+
+
+def workspace(nbytes: int):
+    """A per-thread scratch buffer shared by consecutive kernels on one stream.
+
+    Grows monotonically; returns (pointer, size).  Callers never hold it
+    across an API call, so reuse by the next kernel on the same stream is safe.
+    """
+    t = torch()
+    nbytes = int(max(nbytes, 1 << 20))
+    if _ws.buf is None or _ws.buf.numel() < nbytes:
+        _ws.buf = t.empty(nbytes + (nbytes >> 2), dtype=t.uint8, device=device())
+    return _ws.buf.data_ptr(), _ws.buf.numel()
+
+
+def reserve_workspace(nbytes: int) -> None:
+    workspace(nbytes)

@@ -1,0 +1,160 @@
+// C-ABI entry points for Convolution (functions.py:152-214) and Affine
+// (functions.py:82-119).  Each call builds an implicit-GEMM problem and runs it
+// on the tcgen05 kernel when the shape is eligible (fp16, 16-byte aligned
+// rows), otherwise on the SIMT kernel (fp32 policy, odd channel counts).
+#include "gemm.cuh"
+
+using namespace nnl;
+
+static int check_conv(const nnl_conv_shape* cs) {
+  if (!cs) return fail(NNL_ERR_INVALID_ARGUMENT, "null conv shape");
+  if (cs->n < 0 || cs->h <= 0 || cs->w <= 0 || cs->c <= 0 || cs->k <= 0 || cs->r <= 0 || cs->s <= 0)
+    return fail(NNL_ERR_SHAPE_MISMATCH, "bad conv extents");
+  if (cs->h + 2 * cs->pad_h < cs->r || cs->w + 2 * cs->pad_w < cs->s)
+    return fail(NNL_ERR_KERNEL_TOO_LARGE, "window exceeds padded extent");
+  if (cs->p != (cs->h + 2 * cs->pad_h - cs->r) / cs->stride_h + 1 ||
+      cs->q != (cs->w + 2 * cs->pad_w - cs->s) / cs->stride_w + 1)
+    return fail(NNL_ERR_SHAPE_MISMATCH, "output extent mismatch");
+  return NNL_OK;
+}
+
+static int run_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (pb.M <= 0 || pb.N <= 0) return NNL_OK;
+  if (g_tc_enabled && tc_eligible(pb, dtype)) {
+    int rc = tc_gemm(pb, dtype, ws, ws_bytes, st);
+    if (rc != NNL_ERR_UNSUPPORTED) return rc;
+  }
+  if (pb.stats) return fail(NNL_ERR_UNSUPPORTED, "BN statistics epilogue needs the tcgen05 path");
+  return simt_gemm(pb, dtype, ws, ws_bytes, st);
+}
+
+static size_t gemm_ws(const GemmProblem& pb, int dtype) {
+  size_t a = simt_ws_bytes(pb);
+  size_t b = tc_eligible(pb, dtype) ? tc_ws_bytes(pb) : 0;
+  return a > b ? a : b;
+}
+
+static GemmProblem conv_problem(const nnl_conv_shape* cs, int mode) {
+  GemmProblem pb = {};
+  pb.mode = mode;
+  pb.g = make_geom(*cs);
+  set_extent(pb);
+  return pb;
+}
+
+extern "C" {
+
+size_t nnl_conv2d_workspace_size(const nnl_conv_shape* cs, int dtype, int pass) {
+  if (check_conv(cs)) return 0;
+  GemmProblem pb = conv_problem(cs, pass);
+  size_t w = gemm_ws(pb, dtype);
+  if (pass == kWgrad) {
+    size_t b = bias_grad_ws_bytes((int64_t)cs->n * cs->p * cs->q, cs->k);
+    if (b > w) w = b;
+  }
+  return w + 1024;
+}
+
+int32_t nnl_conv2d_stat_rows(const nnl_conv_shape* cs, int dtype) {
+  if (check_conv(cs)) return 0;
+  GemmProblem pb = conv_problem(cs, kFprop);
+  if (!g_tc_enabled || !tc_eligible(pb, dtype)) return 0;
+  return tc_stat_rows(pb, dtype);
+}
+
+int nnl_conv2d_fwd(const nnl_conv_shape* cs, int dtype, const void* x, const void* w,
+                   const void* b, void* y, float* stat_partials, void* ws, size_t ws_bytes,
+                   void* stream) {
+  int rc = check_conv(cs);
+  if (rc) return rc;
+  GemmProblem pb = conv_problem(cs, kFprop);
+  pb.a = x; pb.b = w; pb.bias = b; pb.out = y; pb.stats = stat_partials;
+  return run_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
+}
+
+int nnl_conv2d_bwd_data(const nnl_conv_shape* cs, int dtype, const void* dy, const void* w,
+                        void* dx, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_conv(cs);
+  if (rc) return rc;
+  GemmProblem pb = conv_problem(cs, kDgrad);
+  pb.a = dy; pb.b = w; pb.out = dx; pb.acc = accumulate;
+  return run_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
+}
+
+int nnl_conv2d_bwd_weight(const nnl_conv_shape* cs, int dtype, const void* x, const void* dy,
+                          void* dw, int acc_w, void* db, int acc_b, int32_t* nonfinite, void* ws,
+                          size_t ws_bytes, void* stream) {
+  int rc = check_conv(cs);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (dw) {
+    GemmProblem pb = conv_problem(cs, kWgrad);
+    pb.a = dy; pb.b = x; pb.out = dw; pb.acc = acc_w; pb.nonfinite = nonfinite;
+    rc = run_gemm(pb, dtype, ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  if (db) {
+    rc = bias_grad(dtype, (int64_t)cs->n * cs->p * cs->q, cs->k, dy, db, acc_b, nonfinite, ws,
+                   ws_bytes, st);
+    if (rc) return rc;
+  }
+  return NNL_OK;
+}
+
+int nnl_affine_fwd(int dtype, int64_t batch, int64_t in_f, int64_t in_c, int64_t out_f, const void* x,
+                   const void* w, const void* b, void* y, void* ws, size_t ws_bytes, void* stream) {
+  GemmProblem pb = {};
+  pb.mode = kFprop;
+  pb.g = affine_geom(batch, in_f, in_c, out_f);
+  set_extent(pb);
+  pb.a = x; pb.b = w; pb.bias = b; pb.out = y;
+  return run_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
+}
+
+int nnl_affine_bwd_data(int dtype, int64_t batch, int64_t in_f, int64_t in_c, int64_t out_f, const void* dy,
+                        const void* w, void* dx, int accumulate, void* ws, size_t ws_bytes,
+                        void* stream) {
+  GemmProblem pb = {};
+  pb.mode = kDgrad;
+  pb.g = affine_geom(batch, in_f, in_c, out_f);
+  set_extent(pb);
+  pb.a = dy; pb.b = w; pb.out = dx; pb.acc = accumulate;
+  return run_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
+}
+
+int nnl_affine_bwd_weight(int dtype, int64_t batch, int64_t in_f, int64_t in_c, int64_t out_f, const void* x,
+                          const void* dy, void* dw, int acc_w, void* db, int acc_b,
+                          int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc;
+  if (dw) {
+    GemmProblem pb = {};
+    pb.mode = kWgrad;
+    pb.g = affine_geom(batch, in_f, in_c, out_f);
+    set_extent(pb);
+    pb.a = dy; pb.b = x; pb.out = dw; pb.acc = acc_w; pb.out_trans = 1; pb.nonfinite = nonfinite;
+    rc = run_gemm(pb, dtype, ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  if (db) {
+    rc = bias_grad(dtype, batch, out_f, dy, db, acc_b, nonfinite, ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  return NNL_OK;
+}
+
+}  // extern "C"
+
+extern "C" size_t nnl_affine_workspace_size(int dtype, int64_t batch, int64_t in_f, int64_t out_f,
+                                            int pass) {
+  GemmProblem pb = {};
+  pb.mode = pass;
+  pb.g = affine_geom(batch, in_f, in_f, out_f);
+  set_extent(pb);
+  size_t w = gemm_ws(pb, dtype);
+  if (pass == kWgrad) {
+    size_t b = bias_grad_ws_bytes(batch, out_f);
+    if (b > w) w = b;
+  }
+  return w + 1024;
+}

@@ -1,0 +1,216 @@
+// Multi-tensor solver and all-reduce bucket kernels.
+//
+//   nnl_multi_nonfinite   <- SgdSolver.check_inf_or_nan_grad (solver.py:115-117)
+//   nnl_multi_scale_grad  <- SgdSolver.scale_grad            (solver.py:106-109)
+//   nnl_multi_sgd_update  <- dynamic_step + update           (solver.py:100-104,132-155)
+//   nnl_bucket_*          <- Communicator._reduce fold       (communicator.py:99-105)
+//
+// All of them walk a host-built chunk table (<=4096 elements per chunk) so one
+// launch covers every parameter regardless of size spread (64 .. 2.4M).
+#include "common.cuh"
+
+namespace nnl {
+
+template <typename F>
+__device__ __forceinline__ void for_chunks(const nnl_chunk* __restrict__ chunks, int32_t n_chunks,
+                                           F&& f) {
+  for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
+    const nnl_chunk ch = chunks[ci];
+    for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x) f(ci, ch.slot, ch.start + j);
+  }
+}
+
+__device__ __forceinline__ float load_any(const void* p, int dtype, int64_t i) {
+  return dtype == NNL_F16 ? __half2float(reinterpret_cast<const __half*>(p)[i])
+                          : reinterpret_cast<const float*>(p)[i];
+}
+__device__ __forceinline__ void store_any(void* p, int dtype, int64_t i, float v) {
+  if (dtype == NNL_F16)
+    reinterpret_cast<__half*>(p)[i] = __float2half_rn(v);
+  else
+    reinterpret_cast<float*>(p)[i] = v;
+}
+
+__global__ void k_multi_nonfinite(const nnl_param_slot* __restrict__ slots,
+                                  const nnl_chunk* __restrict__ chunks, int32_t n_chunks,
+                                  int32_t* flag) {
+  int bad = 0;
+  for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
+    bad |= !isfinite(load_any(slots[s].grad, slots[s].dtype, i));
+  });
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_multi_scale(const nnl_param_slot* __restrict__ slots,
+                              const nnl_chunk* __restrict__ chunks, int32_t n_chunks,
+                              float factor) {
+  for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
+    const nnl_param_slot& p = slots[s];
+    store_any(p.grad, p.dtype, i, __fmul_rn(load_any(p.grad, p.dtype, i), factor));
+  });
+}
+
+__global__ void k_multi_sumsq(const nnl_param_slot* __restrict__ slots,
+                              const nnl_chunk* __restrict__ chunks, int32_t n_chunks,
+                              double* out) {
+  double acc = 0.0;
+  for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
+    float g = load_any(slots[s].grad, slots[s].dtype, i);
+    acc += (double)__fmul_rn(g, g);
+  });
+  acc = warp_sum_d(acc);
+  __shared__ double part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    atomicAdd(out, t);
+  }
+}
+
+__global__ void k_multi_update(const nnl_param_slot* __restrict__ slots,
+                               const nnl_chunk* __restrict__ chunks, int32_t n_chunks, float lr,
+                               float momentum, float wd, const nnl_scaler_state* scaler) {
+  float factor = 1.0f;
+  if (scaler) {
+    if (scaler->nonfinite) return;  // SkippedInfNan: bytes stay unchanged
+    factor = (float)(1.0 / scaler->loss_scale);  // np.float32(1.0 / S)
+  }
+  for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
+    const nnl_param_slot& p = slots[s];
+    float g = load_any(p.grad, p.dtype, i);
+    if (scaler) {
+      // scale_grad rounds the unscaled gradient back into grad storage (R10)
+      store_any(p.grad, p.dtype, i, __fmul_rn(g, factor));
+      g = load_any(p.grad, p.dtype, i);
+    }
+    float m = p.master[i];
+    if (wd != 0.f) g = __fadd_rn(g, __fmul_rn(wd, m));
+    float step = __fmul_rn(lr, g);
+    if (p.momentum) {
+      step = __fadd_rn(__fmul_rn(momentum, p.momentum[i]), step);
+      p.momentum[i] = step;
+    }
+    m = __fsub_rn(m, step);
+    p.master[i] = m;
+    store_any(p.data, p.dtype, i, m);
+  });
+}
+
+__global__ void k_scaler_finish(nnl_scaler_state* s) {
+  if (s->nonfinite) {
+    s->loss_scale = s->loss_scale / s->scaling_factor;
+    s->counter = 0;
+    s->applied = 0;
+  } else {
+    if (s->counter > s->interval) {
+      s->loss_scale = s->loss_scale * s->scaling_factor;
+      s->counter = 0;
+    }
+    s->counter += 1;
+    s->applied = 1;
+  }
+  s->nonfinite = 0;
+}
+
+__global__ void k_bucket_pack(const nnl_param_slot* __restrict__ slots,
+                              const nnl_chunk* __restrict__ chunks,
+                              const int64_t* __restrict__ pos, int32_t n_chunks,
+                              float* __restrict__ bucket) {
+  for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
+    const nnl_chunk ch = chunks[ci];
+    const nnl_param_slot& p = slots[ch.slot];
+    for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x)
+      bucket[pos[ci] + j] = load_any(p.grad, p.dtype, ch.start + j);
+  }
+}
+
+__global__ void k_bucket_unpack(const nnl_param_slot* __restrict__ slots,
+                                const nnl_chunk* __restrict__ chunks,
+                                const int64_t* __restrict__ pos, int32_t n_chunks,
+                                const float* __restrict__ bucket, float world, int32_t* flag) {
+  int bad = 0;
+  for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
+    const nnl_chunk ch = chunks[ci];
+    const nnl_param_slot& p = slots[ch.slot];
+    for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x) {
+      float v = __fdiv_rn(bucket[pos[ci] + j], world);  // acc /= f32(n)
+      store_any(p.grad, p.dtype, ch.start + j, v);
+      bad |= !isfinite(load_any(p.grad, p.dtype, ch.start + j));
+    }
+  }
+  if (flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+static int chunk_grid(int32_t n_chunks) { return n_chunks < 148 * 8 ? (n_chunks > 0 ? n_chunks : 1) : 148 * 8; }
+
+}  // namespace nnl
+
+using namespace nnl;
+
+extern "C" {
+
+int nnl_multi_nonfinite(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                        int32_t* flag, void* stream) {
+  if (n_chunks <= 0) return NNL_OK;
+  k_multi_nonfinite<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, n_chunks,
+                                                                        flag);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+int nnl_multi_scale_grad(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                         float factor, void* stream) {
+  if (n_chunks <= 0) return NNL_OK;
+  k_multi_scale<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, n_chunks,
+                                                                    factor);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+int nnl_multi_sumsq(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                    double* out, void* stream) {
+  if (n_chunks <= 0) return NNL_OK;
+  k_multi_sumsq<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, n_chunks,
+                                                                    out);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+int nnl_multi_sgd_update(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
+                         float lr, float momentum, float weight_decay, nnl_scaler_state* scaler,
+                         void* stream) {
+  if (n_chunks <= 0) return NNL_OK;
+  k_multi_update<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(
+      slots, chunks, n_chunks, lr, momentum, weight_decay, scaler);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+int nnl_scaler_finish(nnl_scaler_state* scaler, void* stream) {
+  k_scaler_finish<<<1, 1, 0, as_stream(stream)>>>(scaler);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+int nnl_bucket_pack(const nnl_param_slot* slots, const nnl_chunk* chunks, const int64_t* chunk_pos,
+                    int32_t n_chunks, float* bucket, void* stream) {
+  if (n_chunks <= 0) return NNL_OK;
+  k_bucket_pack<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, chunk_pos,
+                                                                    n_chunks, bucket);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+int nnl_bucket_unpack_mean(const nnl_param_slot* slots, const nnl_chunk* chunks,
+                           const int64_t* chunk_pos, int32_t n_chunks, const float* bucket,
+                           int32_t world, int32_t* nonfinite, void* stream) {
+  if (n_chunks <= 0) return NNL_OK;
+  k_bucket_unpack<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(
+      slots, chunks, chunk_pos, n_chunks, bucket, (float)world, nonfinite);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+}  // extern "C"

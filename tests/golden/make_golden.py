@@ -1,0 +1,275 @@
+"""Generate golden vectors by running the REFERENCE package (nanonnl).
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  The GPU box has no /root/reference, so these
+committed fixtures are what pins both the oracle restatement and the CUDA
+path there.  Inputs are seeded through the reference's own RngState.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import nanonnl as nn
+    import nanonnl.functions as F
+    import nanonnl.parametric as PF
+    from nanonnl import networks
+    from nanonnl.communicator import DataParallelTrainer
+    return nn, F, PF, networks, DataParallelTrainer
+
+
+def fresh(nn, half: bool, seed: int = 0):
+    tc = nn.TypeConfig.HALF if half else nn.TypeConfig.FLOAT
+    nn.set_default_context(nn.ExecutionContext(type_config=tc))
+    reg = nn.ParameterRegistry(seed=seed)
+    return reg
+
+
+def gen_numerics(nn):
+    from nanonnl.tensor import RngState
+    vals = np.array([65520.0, 65519.9, 2.0 ** -25, 2.0 ** -24, 1.0, 1.0 + 2 ** -13, 7e4,
+                     -65504.0, 3.14159, -2.0 ** -20, 0.1, 1e-8, 6.1e-5, np.inf, -np.inf],
+                    dtype=np.float32)
+    rnd = RngState(seed=11).next_uniform((512,), -70000.0, 70000.0)
+    tiny = RngState(seed=12).next_uniform((512,), -1e-4, 1e-4)
+    q = np.array([nn.quantize_f16(float(v)) for v in np.concatenate([vals, rnd, tiny])],
+                 dtype=np.float32)
+    draws = {}
+    for seed, shape, lo, hi in [(0, (64,), 0.0, 1.0), (1, (3, 5, 7), -2.0, 3.0),
+                                (2 ** 40 + 7, (33,), -0.5, 0.5)]:
+        r = RngState(seed=seed)
+        a = r.next_uniform(shape, lo, hi)
+        b = r.next_uniform(shape, lo, hi)
+        draws[f"rng_{seed}"] = np.concatenate([a.ravel(), b.ravel()])
+    return dict(q_in=np.concatenate([vals, rnd, tiny]), q_out=q, **draws)
+
+
+def run_op(nn, build, inputs, half, diff, seed=1.0, f32_from=None):
+    vs = []
+    for i, a in enumerate(inputs):
+        dt = nn.Dtype.F32 if (f32_from is not None and i >= f32_from) else None
+        v = nn.Variable(a.shape, need_grad=(i in diff), dtype=dt)
+        v.d = a
+        vs.append(v)
+    out = build(vs)
+    out.forward()
+    out.backward(seed)
+    res = {"y": out.d.copy()}
+    for i in diff:
+        res[f"g{i}"] = vs[i].g.copy()
+    return res
+
+
+def gen_ops(nn, F):
+    from nanonnl.tensor import RngState
+    rng = RngState(seed=5)
+    out = {}
+    cases = []
+    # (name, builder, input shapes/ranges, diff indices)
+    for half in (False, True):
+        tag = "h" if half else "f"
+        fresh(nn, half)
+        x = rng.next_uniform((4, 6), -1, 1)
+        w = rng.next_uniform((6, 5), -1, 1)
+        b = rng.next_uniform((5,), -1, 1)
+        cases.append((f"affine_{tag}", half, lambda v: F.affine(*v), [x, w, b], [0, 1, 2]))
+        for (cin, cout, k, s, p, hw) in [(3, 4, 3, 1, 1, 7), (2, 3, 3, 2, 1, 8), (4, 2, 1, 2, 0, 6),
+                                         (1, 2, 5, 1, 0, 9), (3, 2, 7, 2, 3, 11)]:
+            x = rng.next_uniform((2, cin, hw, hw), -1, 1)
+            w = rng.next_uniform((cout, cin, k, k), -1, 1)
+            b = rng.next_uniform((cout,), -1, 1)
+            cases.append((f"conv_{tag}_{cin}_{cout}_{k}_{s}_{p}_{hw}", half,
+                          (lambda s_, p_: lambda v: F.convolution(v[0], v[1], v[2], stride=(s_, s_),
+                                                                  pad=(p_, p_)))(s, p),
+                          [x, w, b], [0, 1, 2]))
+        for (k, s, p, ib, hw) in [(2, 2, 0, True, 8), (3, 2, 1, True, 9), (3, 2, 0, False, 8),
+                                  (2, 1, 0, True, 5)]:
+            x = rng.next_uniform((2, 3, hw, hw), -1, 1)
+            x = np.round(x * 4) / 4  # plenty of ties
+            cases.append((f"pool_{tag}_{k}_{s}_{p}_{int(ib)}_{hw}", half,
+                          (lambda k_, s_, p_, ib_: lambda v: F.max_pooling(
+                              v[0], (k_, k_), (s_, s_), ignore_border=ib_, pad=(p_, p_)))(k, s, p, ib),
+                          [x], [0]))
+        x = np.array([[-1.0, 0.0, 2.0, np.nan, -np.inf, np.inf, 1e-9, -1e-9]], dtype=np.float32)
+        cases.append((f"relu_{tag}", half, lambda v: F.relu(v[0]), [x], [0]))
+        lg = rng.next_uniform((6, 10), -3, 3)
+        lab = (np.arange(6) * 7 % 10).astype(np.float32)
+        cases.append((f"sce_{tag}", half, lambda v: F.softmax_cross_entropy(v[0], v[1]), [lg, lab],
+                      [0]))
+        for bs in (True, False):
+            x = rng.next_uniform((3, 4, 5, 5), -2, 2)
+            g = rng.next_uniform((4,), 0.5, 1.5)
+            be = rng.next_uniform((4,), -0.5, 0.5)
+            m = rng.next_uniform((4,), -0.1, 0.1)
+            vv = rng.next_uniform((4,), 0.5, 1.5)
+
+            def bnb(v, bs=bs):
+                return F.batch_normalization(*v, batch_stat=bs)
+
+            cases.append((f"bn_{tag}_{int(bs)}", half, bnb, [x, g, be, m, vv], [0, 1, 2]))
+    for name, half, build, inputs, diff in cases:
+        fresh(nn, half)
+        # BN scale/shift/statistics are F32 as PF.batch_normalization makes them
+        res = run_op(nn, build, inputs, half, diff, seed=1.0,
+                     f32_from=1 if name.startswith("bn_") else None)
+        for i, a in enumerate(inputs):
+            out[f"{name}__x{i}"] = a
+        for k, v in res.items():
+            out[f"{name}__{k}"] = v
+    return out
+
+
+def gen_solver(nn):
+    from nanonnl import DynamicLossScaler, SgdSolver, dynamic_step
+    out = {}
+    # scales [8,8,8,16,16] with interval 2 (reference tests/test_solver.py:175-183)
+    fresh(nn, True)
+    with nn.registry_scope(nn.ParameterRegistry(0)):
+        w = nn.Variable((4,), need_grad=True)
+        w.d = np.array([1.0, -2.0, 0.5, 3.0], dtype=np.float32)
+        s = SgdSolver(0.1).setup({"w": w})
+        sc = DynamicLossScaler(8.0, 2.0, 2)
+        scales, applied, ws = [], [], []
+        grads = [[1, 2, 3, 4], [0.5, 0.25, 1, 2], [np.inf, 1, 1, 1], [1, 1, 1, 1], [2, 2, 2, 2],
+                 [1e5, 1, 1, 1], [0.1, 0.1, 0.1, 0.1], [3, 3, 3, 3]]
+        for g in grads:
+            w.g = np.array(g, dtype=np.float32) * np.float32(sc.loss_scale)
+            o = dynamic_step(sc, s)
+            scales.append(sc.loss_scale)
+            applied.append(o.applied)
+            ws.append(w.d.copy())
+        out.update(seq_grads=np.array(grads, dtype=np.float32), seq_scales=np.array(scales),
+                   seq_applied=np.array(applied), seq_w=np.array(ws))
+        # half master accumulates below the visible resolution (test_solver.py:80-90)
+        w2 = nn.Variable((1,), need_grad=True)
+        w2.d = np.array([1.0], dtype=np.float32)
+        s2 = SgdSolver(2.0 ** -16).setup({"w": w2})
+        vis = []
+        for _ in range(3):
+            w2.g = np.array([1.0], dtype=np.float32)
+            s2.update()
+            vis.append(float(w2.d[0]))
+        out.update(master_w=np.array(vis), master_m=s2.slots["w"].master.copy())
+    return out
+
+
+def gen_lenet(nn, networks, DataParallelTrainer):
+    import nanonnl.functions as F
+    from nanonnl import DynamicLossScaler, SgdSolver, dynamic_step
+    from nanonnl.tensor import RngState
+    out = {}
+    B = 16
+    x = RngState(seed=1).next_uniform((3, B, 1, 28, 28), 0, 1)
+    lab = (np.arange(B) % 10).astype(np.float32)
+    for half in (False, True):
+        tag = "h" if half else "f"
+        fresh(nn, half)
+        with nn.registry_scope(nn.ParameterRegistry(0)) as reg:
+            xv = nn.Variable((B, 1, 28, 28))
+            tv = nn.Variable((B,))
+            logits = networks.lenet(xv, 10)
+            loss = F.softmax_cross_entropy(logits, tv)
+            params = reg.get_parameters()
+            for k, v in params.items():
+                out[f"lenet_{tag}_init__{k}"] = v.d.copy()
+            solver = SgdSolver(0.05).setup(params)
+            sc = DynamicLossScaler(8.0, 2.0, 2000)
+            losses = []
+            for step in range(3):
+                xv.d = x[step]
+                tv.d = lab
+                loss.forward()
+                if half:
+                    loss.backward(grad_seed=sc.loss_scale)
+                    if step == 0:
+                        for k, v in params.items():
+                            out[f"lenet_{tag}_grad0__{k}"] = v.g.copy()
+                    dynamic_step(sc, solver)
+                else:
+                    loss.backward()
+                    if step == 0:
+                        for k, v in params.items():
+                            out[f"lenet_{tag}_grad0__{k}"] = v.g.copy()
+                    solver.update()
+                losses.append(float(loss.d))
+            out[f"lenet_{tag}_losses"] = np.array(losses)
+            for k, v in params.items():
+                out[f"lenet_{tag}_final__{k}"] = v.d.copy()
+    out["lenet_x"] = x
+    out["lenet_labels"] = lab
+
+    # DataParallelTrainer K=2 on LeNet (F32 and Half, dynamic scaling)
+    def build(bs):
+        xv = nn.Variable((bs, 1, 28, 28))
+        tv = nn.Variable((bs,))
+        return {"x": xv, "label": tv, "loss": F.softmax_cross_entropy(networks.lenet(xv, 10), tv)}
+
+    for half in (False, True):
+        tag = "h" if half else "f"
+        fresh(nn, half)
+        tr = DataParallelTrainer(2, B, build, lr=0.05, seed=0,
+                                 loss_scaling=DynamicLossScaler(8.0, 2.0, 2000) if half else None)
+        losses = [tr.step(x[i], lab) for i in range(2)]
+        out[f"dp2_{tag}_losses"] = np.array(losses)
+        for k, v in tr.rank0.registry.get_parameters().items():
+            out[f"dp2_{tag}_final__{k}"] = v.d.copy()
+    return out
+
+
+def gen_mlp(nn, networks):
+    import nanonnl.functions as F
+    from nanonnl import SgdSolver
+    from nanonnl.tensor import RngState
+    out = {}
+    fresh(nn, False)
+    B = 64
+    x = RngState(seed=1).next_uniform((2, B, 784), 0, 1)
+    lab = (np.arange(B) % 10).astype(np.float32)
+    with nn.registry_scope(nn.ParameterRegistry(0)) as reg:
+        xv = nn.Variable((B, 784))
+        tv = nn.Variable((B,))
+        loss = F.softmax_cross_entropy(networks.mlp(xv, 10, hidden=(256,)), tv)
+        params = reg.get_parameters()
+        solver = SgdSolver(0.1).setup(params)
+        losses = []
+        for s in range(2):
+            xv.d = x[s]
+            tv.d = lab
+            loss.forward()
+            loss.backward()
+            solver.update()
+            losses.append(float(loss.d))
+        out["mlp_losses"] = np.array(losses)
+        for k, v in params.items():
+            out[f"mlp_final__{k}"] = v.d.copy()
+    out["mlp_x"] = x
+    out["mlp_labels"] = lab
+    return out
+
+
+def main():
+    nn, F, PF, networks, DPT = _ref()
+    np.savez_compressed(os.path.join(HERE, "numerics.npz"), **gen_numerics(nn))
+    np.savez_compressed(os.path.join(HERE, "ops.npz"), **gen_ops(nn, F))
+    np.savez_compressed(os.path.join(HERE, "solver.npz"), **gen_solver(nn))
+    np.savez_compressed(os.path.join(HERE, "lenet.npz"), **gen_lenet(nn, networks, DPT))
+    np.savez_compressed(os.path.join(HERE, "mlp.npz"), **gen_mlp(nn, networks))
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()

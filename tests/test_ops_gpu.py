@@ -1,0 +1,164 @@
+"""Per-operator parity of the CUDA path (through the C ABI) against the
+reference's golden vectors and the oracle on identical inputs."""
+
+import numpy as np
+import pytest
+
+from oracle import nnl_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def close(a, b, rtol, atol):
+    np.testing.assert_allclose(np.asarray(a, np.float64), np.asarray(b, np.float64), rtol=rtol,
+                               atol=atol, equal_nan=True)
+
+
+def _ctx(nn, half):
+    tc = nn.TypeConfig.HALF if half else nn.TypeConfig.FLOAT
+    nn.set_default_context(nn.ExecutionContext(type_config=tc))
+
+
+def _build(nn, name, vs):
+    import paper_2102_06725_b200.functions as F
+    kind = name.split("_")[0]
+    if kind == "affine":
+        return F.affine(*vs)
+    if kind == "conv":
+        _, _, cin, cout, k, s, p, hw = name.split("_")
+        return F.convolution(*vs, stride=(int(s), int(s)), pad=(int(p), int(p)))
+    if kind == "pool":
+        _, _, k, s, p, ib, hw = name.split("_")
+        return F.max_pooling(vs[0], (int(k), int(k)), (int(s), int(s)),
+                             ignore_border=bool(int(ib)), pad=(int(p), int(p)))
+    if kind == "relu":
+        return F.relu(vs[0])
+    if kind == "sce":
+        return F.softmax_cross_entropy(*vs)
+    if kind == "bn":
+        return F.batch_normalization(*vs, batch_stat=bool(int(name.split("_")[2])))
+    raise KeyError(name)
+
+
+def _cases(g):
+    return sorted({k.split("__")[0] for k in g})
+
+
+def test_numerics_bit_exact(nnl, golden):
+    g = golden("numerics")
+    from paper_2102_06725_b200.tensor import quantize_f16_array
+    q = quantize_f16_array(g["q_in"])
+    m = ~np.isnan(g["q_out"])
+    assert np.array_equal(q[m].view(np.uint32), g["q_out"][m].view(np.uint32))
+    for seed, shape, lo, hi in [(0, (64,), 0.0, 1.0), (1, (3, 5, 7), -2.0, 3.0),
+                                (2 ** 40 + 7, (33,), -0.5, 0.5)]:
+        r = nnl.RngState(seed)
+        got = np.concatenate([r.next_uniform(shape, lo, hi).ravel(),
+                              r.next_uniform(shape, lo, hi).ravel()])
+        assert np.array_equal(got.view(np.uint32), g[f"rng_{seed}"].view(np.uint32))
+
+
+def test_ops_match_reference_golden(nnl, golden):
+    g = golden("ops")
+    for name in _cases(g):
+        half = name.split("_")[1] == "h"
+        _ctx(nnl, half)
+        kind = name.split("_")[0]
+        diff = [0, 1, 2] if kind in ("affine", "conv", "bn") else [0]
+        xs = []
+        i = 0
+        while f"{name}__x{i}" in g:
+            xs.append(g[f"{name}__x{i}"])
+            i += 1
+        vs = []
+        for j, a in enumerate(xs):
+            dt = nnl.Dtype.F32 if (kind == "bn" and j >= 1) else None
+            v = nnl.Variable(a.shape, need_grad=(j in diff), dtype=dt)
+            v.d = a
+            vs.append(v)
+        y = _build(nnl, name, vs)
+        y.forward()
+        y.backward(1.0)
+        tol = dict(rtol=2e-3, atol=2e-3) if half else dict(rtol=1e-5, atol=1e-5)
+        close(y.d, g[f"{name}__y"], **tol)
+        for j in diff:
+            close(vs[j].g, g[f"{name}__g{j}"], **tol)
+
+
+def test_maxpool_indices_bit_exact_vs_oracle(nnl):
+    """Integer outputs (argmax) are bit-exact on identical inputs."""
+    import paper_2102_06725_b200.functions as F
+    _ctx(nnl, True)
+    rng = np.random.default_rng(3)
+    x = (np.round(rng.uniform(-2, 2, (4, 8, 13, 13)) * 2) / 2).astype(np.float32)
+    x[0, 0, 0, :4] = np.nan
+    v = nnl.Variable(x.shape, need_grad=True)
+    v.d = x
+    y = F.max_pooling(v, (3, 3), (2, 2), pad=(1, 1))
+    y.forward()
+    want_y, want_arg = O.maxpool_forward(O.q16(x), (3, 3), (2, 2), (1, 1))
+    got_arg = y.parent.state["argmax"].cpu().numpy().reshape(4, 7, 7, 8).transpose(0, 3, 1, 2)
+    assert np.array_equal(got_arg, want_arg)
+    close(y.d, O.q16(want_y), 0, 0)
+    gy = O.q16(rng.uniform(-1, 1, y.shape).astype(np.float32))
+    y.backward(1.0)  # seeds ones; check the scatter with a non-uniform grad below
+    y.g = gy
+    v.grad.fill(0.0)
+    y.parent.impl.backward(y.parent, [y.grad], [v.grad], [False])
+    want_gx = O.q16(O.maxpool_backward(gy, want_arg, x.shape, (3, 3), (2, 2), (1, 1)))
+    close(v.g, want_gx, 0, 0)
+
+
+def test_label_out_of_range_raises(nnl):
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200.errors import LabelOutOfRange
+    lg = nnl.Variable((2, 3))
+    lb = nnl.Variable((2,))
+    y = F.softmax_cross_entropy(lg, lb)
+    lg.d = np.zeros((2, 3), np.float32)
+    lb.d = np.array([0, 3], np.float32)
+    with pytest.raises(LabelOutOfRange):
+        y.forward()
+    lb.d = np.array([0, 1.5], np.float32)
+    with pytest.raises(LabelOutOfRange):
+        y.forward()
+    lb.d = np.array([0, 2], np.float32)
+    y.forward()
+
+
+def test_relu_nan_and_inf_gate(nnl):
+    """R6: forward keeps NaN; backward multiplies, inf * 0 = NaN."""
+    import paper_2102_06725_b200.functions as F
+    v = nnl.Variable((3,), need_grad=True)
+    v.d = np.array([-1.0, 0.0, 2.0], np.float32)
+    y = F.relu(v)
+    y.forward()
+    y.backward(np.inf)
+    g = v.g
+    assert np.isnan(g[0]) and np.isnan(g[1]) and np.isinf(g[2])
+
+
+@pytest.mark.parametrize("half", [False, True])
+@pytest.mark.parametrize("geom", [(3, 8, 3, 1, 1, 9), (16, 16, 5, 1, 0, 12), (8, 4, 3, 2, 1, 10),
+                                  (4, 8, 1, 2, 0, 7), (3, 4, 7, 2, 3, 15)])
+def test_conv_random_vs_oracle(nnl, half, geom):
+    import paper_2102_06725_b200.functions as F
+    _ctx(nnl, half)
+    cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(hash(geom) % 1000)
+    x = rng.uniform(-1, 1, (3, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.5, 0.5, (cout, cin, k, k)).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, (cout,)).astype(np.float32)
+    vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, b)]
+    for v, a in zip(vs, (x, w, b)):
+        v.d = a
+    y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+    y.forward()
+    y.backward(1.0)
+    ov = [O.Var(a, half=half, need_grad=True) for a in (x, w, b)]
+    oy = O.conv2d(*ov, (s, s), (p, p), half)
+    O.backward(oy, 1.0)
+    tol = dict(rtol=1e-2, atol=1e-2) if half else dict(rtol=1e-5, atol=1e-5)
+    close(y.d, oy.value, **tol)
+    for v, o in zip(vs, ov):
+        close(v.g, o.grad, **tol)

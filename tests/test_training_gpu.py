@@ -1,0 +1,218 @@
+"""End-to-end parity: whole training steps on the GPU against the reference's
+golden trajectories and the oracle (same seeds, same inputs)."""
+
+import numpy as np
+import pytest
+
+from oracle import nnl_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def close(a, b, rtol, atol):
+    np.testing.assert_allclose(np.asarray(a, np.float64), np.asarray(b, np.float64), rtol=rtol,
+                               atol=atol, equal_nan=True)
+
+
+def _ctx(nn, half):
+    tc = nn.TypeConfig.HALF if half else nn.TypeConfig.FLOAT
+    nn.set_default_context(nn.ExecutionContext(type_config=tc))
+
+
+@pytest.mark.parametrize("half", [False, True])
+@pytest.mark.parametrize("clear", [False, True])
+def test_lenet_steps_match_reference(nnl, golden, half, clear):
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    g = golden("lenet")
+    tag = "h" if half else "f"
+    _ctx(nnl, half)
+    with nnl.registry_scope(nnl.ParameterRegistry(0)) as reg:
+        xv = nnl.Variable((16, 1, 28, 28))
+        tv = nnl.Variable((16,))
+        loss = F.softmax_cross_entropy(networks.lenet(xv, 10), tv)
+        params = reg.get_parameters()
+        for k, v in params.items():  # R12: bit-identical initial weights
+            assert np.array_equal(v.d, g[f"lenet_{tag}_init__{k}"]), k
+        solver = nnl.SgdSolver(0.05).setup(params)
+        sc = nnl.DynamicLossScaler(8.0, 2.0, 2000)
+        losses = []
+        for s in range(3):
+            xv.d = g["lenet_x"][s]
+            tv.d = g["lenet_labels"]
+            loss.forward(clear_buffer=clear)
+            loss.backward(grad_seed=sc.loss_scale if half else 1.0, clear_buffer=clear)
+            if s == 0:
+                tol = dict(rtol=2e-2, atol=2e-2) if half else dict(rtol=1e-4, atol=1e-5)
+                for k, v in params.items():
+                    close(v.g, g[f"lenet_{tag}_grad0__{k}"], **tol)
+            if half:
+                assert nnl.dynamic_step(sc, solver).applied
+            else:
+                solver.update()
+            losses.append(float(loss.d))
+    tol = dict(rtol=2e-3, atol=2e-3) if half else dict(rtol=1e-5, atol=1e-6)
+    close(losses, g[f"lenet_{tag}_losses"], **tol)
+    for k, v in params.items():
+        close(v.d, g[f"lenet_{tag}_final__{k}"], rtol=1e-2 if half else 1e-5,
+              atol=2e-3 if half else 1e-6)
+
+
+def test_mlp_fp32_matches_reference(nnl, golden):
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    g = golden("mlp")
+    _ctx(nnl, False)
+    with nnl.registry_scope(nnl.ParameterRegistry(0)) as reg:
+        xv = nnl.Variable((64, 784))
+        tv = nnl.Variable((64,))
+        loss = F.softmax_cross_entropy(networks.mlp(xv, 10, hidden=(256,)), tv)
+        solver = nnl.SgdSolver(0.1).setup(reg.get_parameters())
+        losses = []
+        for s in range(2):
+            xv.d = g["mlp_x"][s]
+            tv.d = g["mlp_labels"]
+            loss.forward()
+            loss.backward()
+            solver.update()
+            losses.append(float(loss.d))
+        close(losses, g["mlp_losses"], rtol=1e-5, atol=1e-6)
+        for k, v in reg.get_parameters().items():
+            close(v.d, g[f"mlp_final__{k}"], rtol=1e-5, atol=1e-6)
+
+
+def test_dynamic_scaler_sequence_matches_reference(nnl, golden):
+    g = golden("solver")
+    _ctx(nnl, True)
+    w = nnl.Variable((4,), need_grad=True)
+    w.d = np.array([1.0, -2.0, 0.5, 3.0], np.float32)
+    s = nnl.SgdSolver(0.1).setup({"w": w})
+    sc = nnl.DynamicLossScaler(8.0, 2.0, 2)
+    for i, gr in enumerate(g["seq_grads"]):
+        w.g = gr * np.float32(sc.loss_scale)
+        out = nnl.dynamic_step(sc, s)
+        assert out.applied == bool(g["seq_applied"][i])          # integer decision: exact
+        assert sc.loss_scale == g["seq_scales"][i]
+        assert np.array_equal(w.d, g["seq_w"][i])                # bitwise
+
+
+def test_device_scaler_matches_host_scaler(nnl, golden):
+    """The sync-free device state machine reproduces dynamic_step exactly."""
+    g = golden("solver")
+    _ctx(nnl, True)
+    w = nnl.Variable((4,), need_grad=True)
+    w.d = np.array([1.0, -2.0, 0.5, 3.0], np.float32)
+    s = nnl.SgdSolver(0.1).setup({"w": w})
+    dsc = nnl.DeviceLossScaler(nnl.DynamicLossScaler(8.0, 2.0, 2))
+    for i, gr in enumerate(g["seq_grads"]):
+        w.g = gr * np.float32(dsc.snapshot().loss_scale)
+        s.dynamic_update(dsc, check=True)
+        assert dsc.last_applied() == bool(g["seq_applied"][i])
+        assert dsc.snapshot().loss_scale == g["seq_scales"][i]
+        assert np.array_equal(w.d, g["seq_w"][i])
+
+
+def test_half_master_accumulates(nnl, golden):
+    g = golden("solver")
+    _ctx(nnl, True)
+    w = nnl.Variable((1,), need_grad=True)
+    w.d = np.array([1.0], np.float32)
+    s = nnl.SgdSolver(2.0 ** -16).setup({"w": w})
+    vis = []
+    for _ in range(3):
+        w.g = np.array([1.0], np.float32)
+        s.update()
+        vis.append(float(w.d[0]))
+    assert vis == list(g["master_w"])
+    assert np.array_equal(s.master_values("w"), g["master_m"])
+
+
+@pytest.mark.parametrize("half", [False, True])
+def test_dp2_inprocess_matches_reference(nnl, golden, half):
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    from paper_2102_06725_b200.communicator import DataParallelTrainer
+    g = golden("lenet")
+    tag = "h" if half else "f"
+    _ctx(nnl, half)
+
+    def build(bs):
+        xv = nnl.Variable((bs, 1, 28, 28))
+        tv = nnl.Variable((bs,))
+        return {"x": xv, "label": tv,
+                "loss": F.softmax_cross_entropy(networks.lenet(xv, 10), tv)}
+
+    tr = DataParallelTrainer(2, 16, build, lr=0.05, seed=0,
+                             loss_scaling=nnl.DynamicLossScaler(8.0, 2.0, 2000) if half else None)
+    losses = [tr.step(g["lenet_x"][i], g["lenet_labels"]) for i in range(2)]
+    tol = dict(rtol=2e-3, atol=2e-3) if half else dict(rtol=1e-5, atol=1e-6)
+    close(losses, g[f"dp2_{tag}_losses"], **tol)
+    for k, v in tr.rank0.registry.get_parameters().items():
+        close(v.d, g[f"dp2_{tag}_final__{k}"], rtol=1e-2 if half else 1e-5,
+              atol=2e-3 if half else 1e-6)
+
+
+def test_static_equals_dynamic_bitwise(nnl):
+    """Reference property (tests/test_graph.py:238-260)."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    x = O.uniform(3, 0, (8, 1, 28, 28), 0, 1)
+    lab = (np.arange(8) % 10).astype(np.float32)
+    outs = []
+    for mode in (nnl.Mode.STATIC, nnl.Mode.DYNAMIC):
+        nnl.set_default_context(nnl.ExecutionContext(mode=mode, type_config=nnl.TypeConfig.HALF))
+        with nnl.registry_scope(nnl.ParameterRegistry(0)) as reg:
+            xv = nnl.Variable(x.shape)
+            tv = nnl.Variable(lab.shape)
+            xv.d = x
+            tv.d = lab
+            loss = F.softmax_cross_entropy(networks.lenet(xv, 10), tv)
+            loss.forward()
+            loss.backward(8.0)
+            outs.append((loss.d.copy(), reg.get_parameters()["conv1/W"].g.copy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def _resnet_oracle_step(builder, x, lab, half, lr, n_classes):
+    tr = O.Trainer(lambda m, a, t: m.sce(builder(m, a, n_classes), t), 1, x.shape[0], lr,
+                   seed=0, half=half, scaler=O.Scaler(8.0, 2.0, 2000) if half else None)
+    loss = tr.step(x, lab)
+    return loss, tr
+
+
+@pytest.mark.parametrize("half", [False, True])
+def test_resnet18_cifar_step_vs_oracle(nnl, half):
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    _ctx(nnl, half)
+    B = 4
+    x = O.uniform(1, 0, (B, 3, 32, 32), 0, 1)
+    lab = (np.arange(B) % 10).astype(np.float32)
+    with nnl.registry_scope(nnl.ParameterRegistry(0)) as reg:
+        xv = nnl.Variable(x.shape)
+        tv = nnl.Variable(lab.shape)
+        loss = F.softmax_cross_entropy(networks.resnet18_cifar(xv, 10), tv)
+        solver = nnl.SgdSolver(0.1).setup(reg.get_parameters())
+        sc = nnl.DynamicLossScaler(8.0, 2.0, 2000)
+        xv.d = x
+        tv.d = lab
+        loss.forward(clear_buffer=True)
+        loss.backward(grad_seed=sc.loss_scale if half else 1.0, clear_buffer=True)
+        if half:
+            assert nnl.dynamic_step(sc, solver).applied
+        else:
+            solver.update()
+        grads = {k: v.g for k, v in reg.get_parameters().items()}  # unscaled, as the oracle's
+        got = float(loss.d)
+        weights = {k: v.d for k, v in reg.get_parameters().items()}
+    want, tr = _resnet_oracle_step(O.resnet18_cifar, x, lab, half, 0.1, 10)
+    assert abs(got - want) <= (2e-2 if half else 1e-4) * max(1, abs(want))
+    params = tr.models[0].trainable()
+    assert set(params) == set(grads)
+    for k, v in params.items():
+        scale = np.abs(v.grad).max() + 1e-6
+        # gradients through 20 BN layers: compare relative to each tensor's scale
+        err = np.abs(grads[k] - v.grad).max() / scale
+        assert err < (5e-2 if half else 1e-3), (k, err)
+        close(weights[k], v.value, rtol=1e-2 if half else 1e-4, atol=1e-2 if half else 1e-5)
