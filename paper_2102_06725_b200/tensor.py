@@ -129,7 +129,9 @@ class NdArray:
         if src.shape != self.shape:
             raise ShapeMismatch(f"cannot write shape {src.shape} into {self.shape}")
         t = _lib.torch()
-        host = t.from_numpy(np.ascontiguousarray(src))
+        if not (src.flags.c_contiguous and src.flags.writeable):
+            src = np.array(src, dtype=np.float32, order="C")
+        host = t.from_numpy(src)
         dev = host.to(self._t.device, non_blocking=host.is_pinned())
         self.write_f32_device(dev)
 

@@ -1,0 +1,133 @@
+"""The tcgen05 implicit-GEMM path (fp16 shapes with 64-multiple channels,
+the im2col stem, affine layers) against the oracle and the SIMT kernel."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import nnl_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CONV = [  # (B, cin, cout, k, stride, pad, hw)
+    (2, 64, 128, 1, 1, 0, 8),      # 1x1 s1: TMA A / TMA B
+    (2, 64, 64, 3, 1, 1, 8),       # 3x3 gather, BN=64
+    (3, 128, 128, 3, 2, 1, 9),     # strided 3x3, ragged M tail
+    (2, 64, 256, 1, 2, 0, 10),     # 1x1 s2 (downsample)
+    (2, 3, 64, 7, 2, 3, 20),       # stem: explicit im2col
+    (4, 256, 64, 1, 1, 0, 7),      # 1x1 reduce, 7x7 maps
+]
+
+
+def _half(nn):
+    nn.set_default_context(nn.ExecutionContext(type_config=nn.TypeConfig.HALF))
+
+
+def _rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b).max() / (np.abs(b).max() + 1e-6)
+
+
+@pytest.mark.parametrize("geom", CONV)
+def test_conv_tc_vs_oracle(nnl, geom):
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    b, cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(cin * 7 + cout + k)
+    x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.2, 0.2, (cout, cin, k, k)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, (cout,)).astype(np.float32)
+    vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+    for v, a in zip(vs, (x, w, bias)):
+        v.d = a
+    y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+    gy = O.q16(rng.uniform(-1, 1, y.shape).astype(np.float32))
+    before = _lib.lib().nnl_launch_count(0)
+    y.forward()
+    y.g = gy
+    node = y.parent
+    for v in vs:
+        v.grad.fill(0.0)
+    node.impl.backward(node, [y.grad], [v.grad for v in vs], [False] * 3)
+    ov = [O.Var(a, half=True, need_grad=True) for a in (x, w, bias)]
+    oy = O.conv2d(*ov, (s, s), (p, p), True)
+    gxs = oy.parent.bwd([gy], [True, True, True])
+    assert _rel_err(y.d, oy.value) < 4e-3
+    for v, want in zip(vs, gxs):
+        assert _rel_err(v.g, O.q16(want)) < 4e-3, (geom, v.shape)
+    assert _lib.lib().nnl_launch_count(0) > before
+
+
+def test_conv_tc_matches_simt_kernel(nnl):
+    """Same inputs through both kernels (tensor cores vs SIMT fp32 accumulation)."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, (2, 64, 12, 12)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (128, 64, 3, 3)).astype(np.float32)
+    bias = np.zeros(128, np.float32)
+    outs = []
+    for tc in (1, 0):
+        prev = _lib.lib().nnl_set_tc_enabled(tc)
+        try:
+            vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+            for v, a in zip(vs, (x, w, bias)):
+                v.d = a
+            y = F.convolution(*vs, stride=(1, 1), pad=(1, 1))
+            y.forward()
+            y.backward(1.0)
+            outs.append([y.d, vs[0].g, vs[1].g])
+        finally:
+            _lib.lib().nnl_set_tc_enabled(prev)
+    for a, b in zip(*outs):
+        assert _rel_err(a, b) < 2e-3
+
+
+def test_conv_stats_epilogue(nnl):
+    """BN partial statistics from the conv epilogue equal column sums of the
+    rounded output."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    rng = np.random.default_rng(1)
+    x = rng.uniform(-1, 1, (3, 64, 9, 9)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (64, 64, 3, 3)).astype(np.float32)
+    vs = [nnl.Variable(a.shape) for a in (x, w, np.zeros(64, np.float32))]
+    for v, a in zip(vs, (x, w, np.zeros(64, np.float32))):
+        v.d = a
+    y = F.convolution(*vs, stride=(1, 1), pad=(1, 1))
+    y.parent.state["emit_stats"] = True
+    y.forward()
+    st = y.parent.state["stats"].cpu().numpy()
+    rows = y.parent.state["stat_rows"]
+    parts = st[: rows * 2 * 64].reshape(rows, 2, 64)
+    yd = y.d.transpose(0, 2, 3, 1).reshape(-1, 64).astype(np.float64)
+    np.testing.assert_allclose(parts[:, 0].sum(0), yd.sum(0), rtol=1e-4, atol=1e-3)
+    np.testing.assert_allclose(parts[:, 1].sum(0), (yd ** 2).sum(0), rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("dims", [(32, 128, 64), (16, 256, 1000), (256, 2048, 1000)])
+def test_affine_tc_vs_oracle(nnl, dims):
+    import paper_2102_06725_b200.functions as F
+    _half(nnl)
+    bsz, i, o = dims
+    rng = np.random.default_rng(i + o)
+    x = rng.uniform(-1, 1, (bsz, i)).astype(np.float32)
+    w = rng.uniform(-0.05, 0.05, (i, o)).astype(np.float32)
+    bias = rng.uniform(-0.1, 0.1, (o,)).astype(np.float32)
+    vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+    for v, a in zip(vs, (x, w, bias)):
+        v.d = a
+    y = F.affine(*vs)
+    y.forward()
+    y.backward(1.0)
+    ov = [O.Var(a, half=True, need_grad=True) for a in (x, w, bias)]
+    oy = O.affine(*ov, True)
+    O.backward(oy, 1.0)
+    assert _rel_err(y.d, oy.value) < 4e-3
+    for v, o_ in zip(vs, ov):
+        assert _rel_err(v.g, o_.grad) < 4e-3
