@@ -366,8 +366,9 @@ class DataParallelTrainer:
 
     def _work(self, rep: _Replica, rank: int, x_batch, label_batch, all_reduce) -> object:
         lo = rank * self.shard_size
-        rep.handles["x"].d = x_batch[lo:lo + self.shard_size]
-        rep.handles["label"].d = label_batch[lo:lo + self.shard_size]
+        if x_batch is not None:
+            rep.handles["x"].d = x_batch[lo:lo + self.shard_size]
+            rep.handles["label"].d = label_batch[lo:lo + self.shard_size]
         loss = rep.handles["loss"]
         loss.forward(clear_buffer=True)
         if rep.dscaler is not None:
@@ -392,8 +393,51 @@ class DataParallelTrainer:
             rep.solver.update()
         return loss
 
-    def step(self, x_batch: np.ndarray, label_batch: np.ndarray) -> float:
-        """One synchronised step; returns the batch loss (mean of shard losses)."""
+    def step_resident(self) -> None:
+        """One step on the inputs already resident on the device: no host
+        transfer and no loss read-back (the benchmark's device-side `value`)."""
+        if self.distributed:
+            rep = self.replicas[0]
+
+            def ar(r):
+                flag = r.dscaler.nonfinite_ptr if r.dscaler is not None else None
+                self.comm.all_reduce([p.grad for p in r.params], division=True,
+                                     nonfinite_ptr=flag)
+
+            self._work(rep, self.ranks[0], None, None, ar)
+        elif self.n_workers == 1:
+            self._work(self.replicas[0], 0, None, None, lambda r: None)
+        else:
+            raise NotImplementedError("step_resident needs one replica per process")
+
+    def step(self, x_batch: np.ndarray, label_batch: np.ndarray, shard: bool = False) -> float:
+        """One synchronised step; returns the batch loss (mean of shard losses).
+
+        ``shard=True`` (extension): under torch.distributed the arrays are
+        already this rank's shard, so no process materialises the global batch.
+        """
+        if shard and self.distributed:
+            rep = self.replicas[0]
+            rep.handles["x"].d = x_batch
+            rep.handles["label"].d = label_batch
+            x_batch = label_batch = None
+            rank = self.ranks[0]
+
+            def ar(r):
+                flag = r.dscaler.nonfinite_ptr if r.dscaler is not None else None
+                self.comm.all_reduce([p.grad for p in r.params], division=True,
+                                     nonfinite_ptr=flag)
+
+            loss = self._work(rep, rank, None, None, ar)
+            t = _lib.torch()
+            lv = t.empty(1, dtype=t.float32, device=_lib.device())
+            _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr, lv.data_ptr(),
+                      _lib.stream())
+            self.comm._dist.all_reduce(lv)
+            return float(lv.item()) / self.n_workers
+        if not self.distributed and self.n_workers == 1:
+            loss = self._work(self.replicas[0], 0, x_batch, label_batch, lambda r: None)
+            return float(loss.d)
         if self.distributed:
             rep = self.replicas[0]
             rank = self.ranks[0]

@@ -1,0 +1,74 @@
+"""CUDA-event timing of individual graph nodes (the build's tracing hook).
+
+When enabled, the engine brackets every node's forward / backward launch
+sequence with CUDA events on the current stream; ``summary()`` then gives
+per-kind device time, and ``gemm_flops`` the algorithmic FLOPs of each
+Convolution / Affine call (2*M*N*K per GEMM pass) for roofline fractions.
+"""
+
+from __future__ import annotations
+
+import contextlib
+from collections import defaultdict
+
+from . import _lib
+
+
+class _Profiler:
+    def __init__(self):
+        self.enabled = False
+        self.records = []  # (kind, phase, flops, bytes, start_event, end_event)
+
+    def reset(self):
+        self.records = []
+
+    @contextlib.contextmanager
+    def region(self, node, phase: str):
+        if not self.enabled:
+            yield
+            return
+        t = _lib.torch()
+        s = t.cuda.Event(enable_timing=True)
+        e = t.cuda.Event(enable_timing=True)
+        s.record()
+        yield
+        e.record()
+        self.records.append((node.kind, phase, gemm_flops(node, phase), s, e))
+
+    def summary(self) -> dict:
+        _lib.torch().cuda.synchronize()
+        out = defaultdict(lambda: {"ms": 0.0, "flops": 0.0, "calls": 0})
+        for kind, phase, flops, s, e in self.records:
+            d = out[f"{kind}.{phase}"]
+            d["ms"] += s.elapsed_time(e)
+            d["flops"] += flops
+            d["calls"] += 1
+        return dict(out)
+
+
+PROFILER = _Profiler()
+
+
+def gemm_flops(node, phase: str) -> float:
+    """Algorithmic FLOPs of the implicit GEMMs a node runs in `phase`."""
+    if node.kind == "Convolution":
+        x = node.inputs[0].shape
+        y = node.outputs[0].shape
+        o, c, kh, kw = node.inputs[1].shape
+        one = 2.0 * y[0] * y[2] * y[3] * o * c * kh * kw
+        if phase == "fwd":
+            return one
+        n = 0
+        if node.inputs[0].need_grad:
+            n += 1
+        if node.inputs[1].need_grad:
+            n += 1
+        return one * n
+    if node.kind == "Affine":
+        b = node.inputs[0].shape[0]
+        i, o = node.inputs[1].shape
+        one = 2.0 * b * i * o
+        if phase == "fwd":
+            return one
+        return one * (int(node.inputs[0].need_grad) + int(node.inputs[1].need_grad))
+    return 0.0
