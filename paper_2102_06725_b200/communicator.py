@@ -40,6 +40,31 @@ __all__ = ["Communicator", "CommunicatorGroup", "DataParallelCommunicator",
            "DataParallelTrainer", "data_parallel_step", "BucketPlan"]
 
 
+def plan_buckets(sizes: list[int], bucket_bytes: int) -> list[list[int]]:
+    """Group consecutive buffers (in list order) into f32 buckets of at least
+    `bucket_bytes` (the last may be smaller).  Pure host logic, shared by the
+    NCCL path and the gloo tests."""
+    groups, cur, size = [], [], 0
+    for i, n in enumerate(sizes):
+        cur.append(i)
+        size += int(n) * 4
+        if size >= bucket_bytes:
+            groups.append(cur)
+            cur, size = [], 0
+    if cur:
+        groups.append(cur)
+    return groups
+
+
+def bucket_layout(sizes: list[int]) -> list[int]:
+    """Element offset of each buffer inside its f32 bucket (concatenation)."""
+    offs, o = [], 0
+    for n in sizes:
+        offs.append(o)
+        o += int(n)
+    return offs
+
+
 class BucketPlan:
     """Packing of a list of gradient NdArrays into one f32 device bucket."""
 
@@ -228,15 +253,8 @@ class DataParallelCommunicator:
         key = tuple(a.ptr for a in buffers)
         plans = self._plans.get(key)
         if plans is None:
-            plans, cur, size = [], [], 0
-            for a in buffers:
-                cur.append(a)
-                size += a.size * 4
-                if size >= self.bucket_bytes:
-                    plans.append(BucketPlan(cur))
-                    cur, size = [], 0
-            if cur:
-                plans.append(BucketPlan(cur))
+            groups = plan_buckets([a.size for a in buffers], self.bucket_bytes)
+            plans = [BucketPlan([buffers[i] for i in g]) for g in groups]
             self._plans[key] = plans
         return plans
 

@@ -33,12 +33,18 @@ class _Profiler:
         s.record()
         yield
         e.record()
-        self.records.append((node.kind, phase, gemm_flops(node, phase), s, e))
+        self.records.append((node.kind, phase, gemm_flops(node, phase), s, e, _describe(node)))
+
+    def per_node(self) -> list[dict]:
+        """One entry per recorded node call, in launch order."""
+        _lib.torch().cuda.synchronize()
+        return [{"kind": k, "phase": ph, "shape": desc, "ms": s.elapsed_time(e), "flops": fl}
+                for k, ph, fl, s, e, desc in self.records]
 
     def summary(self) -> dict:
         _lib.torch().cuda.synchronize()
         out = defaultdict(lambda: {"ms": 0.0, "flops": 0.0, "calls": 0})
-        for kind, phase, flops, s, e in self.records:
+        for kind, phase, flops, s, e, _ in self.records:
             d = out[f"{kind}.{phase}"]
             d["ms"] += s.elapsed_time(e)
             d["flops"] += flops
@@ -47,6 +53,15 @@ class _Profiler:
 
 
 PROFILER = _Profiler()
+
+
+def _describe(node) -> str:
+    ins = "x".join(str(d) for d in node.inputs[0].shape)
+    if node.kind == "Convolution":
+        o, c, kh, kw = node.inputs[1].shape
+        s = node.impl.stride[0]
+        return f"{ins} -> {o} k{kh} s{s}"
+    return ins
 
 
 def gemm_flops(node, phase: str) -> float:
