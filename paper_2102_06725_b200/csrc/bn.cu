@@ -228,86 +228,181 @@ __global__ void __launch_bounds__(1024) k_bn_finalize_bwd(
   }
 }
 
+template <typename T, int V>
+struct VecStore;
+template <typename T>
+struct VecStore<T, 1> {
+  static __device__ __forceinline__ void store(T* p, const T* v) { p[0] = v[0]; }
+};
+template <>
+struct VecStore<__half, 8> {
+  static __device__ __forceinline__ void store(__half* p, const __half* v) {
+    *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(v);
+  }
+};
+template <>
+struct VecStore<float, 8> {
+  static __device__ __forceinline__ void store(float* p, const float* v) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+// Apply kernels use the same (row chunk x channel slab) decomposition as the
+// reductions: each thread owns V channels for the whole launch, so the
+// per-channel constants live in registers and the inner loop has no index
+// division (the first version's int64 `i % C` per element cost 5x).
+constexpr int kUnroll = 4;
+
 // y = q(gamma * ((x - mu) * istd) + beta), then ReLU on the stored value
 template <typename T, int V>
-__global__ void k_bn_fwd_apply(int64_t rows, int32_t c, const T* __restrict__ x,
-                               const float* __restrict__ gamma, const float* __restrict__ beta,
-                               const float* __restrict__ mu, const float* __restrict__ istd,
-                               T* __restrict__ y, int fuse_relu) {
-  const int64_t nvec = rows * c / V;
-  const int cv = c / V;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % cv) * V;
-    float xv[V];
-    VecLoad<T, V>::load(x + i * V, xv);
-    T out[V];
+__global__ void __launch_bounds__(kBnThreads) k_bn_fwd_apply(
+    int64_t rows, int32_t c, int groups, int lanes, int64_t rows_per_block,
+    const T* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
+    const float* __restrict__ mu, const float* __restrict__ istd, T* __restrict__ y,
+    int fuse_relu) {
+  const int g = threadIdx.x % groups, lane = threadIdx.x / groups;
+  const int c0 = (blockIdx.y * groups + g) * V;
+  if (lane >= lanes || c0 >= c) return;
+  float m[V], is[V], ga[V], be[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      float xh = __fmul_rn(__fsub_rn(xv[j], mu[c0 + j]), istd[c0 + j]);
-      float v = __fadd_rn(__fmul_rn(gamma[c0 + j], xh), beta[c0 + j]);
-      T q = Elem<T>::st(v);
-      if (fuse_relu) {
-        float f = Elem<T>::ld(q);
-        q = Elem<T>::st((f > 0.f || f != f) ? f : 0.f);
-      }
-      out[j] = q;
+  for (int j = 0; j < V; ++j) {
+    m[j] = mu[c0 + j];
+    is[j] = istd[c0 + j];
+    ga[j] = gamma[c0 + j];
+    be[j] = beta[c0 + j];
+  }
+  const int64_t r0 = blockIdx.x * rows_per_block;
+  const int64_t r1 = min(r0 + rows_per_block, rows);
+  for (int64_t rb = r0 + lane; rb < r1; rb += (int64_t)lanes * kUnroll) {
+    float xv[kUnroll][V];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t r = rb + (int64_t)u * lanes;
+      if (r < r1) VecLoad<T, V>::load(x + r * c + c0, xv[u]);
     }
-    if (V == 8 && sizeof(T) == 2) {
-      *reinterpret_cast<uint4*>(y + i * V) = *reinterpret_cast<uint4*>(out);
-    } else {
 #pragma unroll
-      for (int j = 0; j < V; ++j) y[i * V + j] = out[j];
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t r = rb + (int64_t)u * lanes;
+      if (r >= r1) break;
+      T out[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float xh = __fmul_rn(__fsub_rn(xv[u][j], m[j]), is[j]);
+        T q = Elem<T>::st(__fadd_rn(__fmul_rn(ga[j], xh), be[j]));
+        if (fuse_relu) {
+          const float f = Elem<T>::ld(q);
+          q = Elem<T>::st((f > 0.f || f != f) ? f : 0.f);
+        }
+        out[j] = q;
+      }
+      VecStore<T, V>::store(y + r * c + c0, out);
     }
   }
 }
 
 // gx = (g/n) * (n*gy - gbeta - xhat*ggamma), g = gamma*istd (functions.py:424-432)
-// eval mode: gx = g * gy (functions.py:433-434)
+// eval mode: gx = g * gy (functions.py:433-434).  With `bias_part` the block
+// also emits column sums of the ROUNDED gx: the gradient of the producing
+// convolution's bias (functions.py:211-212), saving a separate pass.
 template <typename T, int V>
-__global__ void k_bn_bwd_apply(int64_t rows, int32_t c, const T* __restrict__ x,
-                               const T* __restrict__ dy, const T* __restrict__ relu_out,
-                               const float* __restrict__ gamma, const float* __restrict__ mu,
-                               const float* __restrict__ istd, const float* __restrict__ gsum,
-                               int batch_stat, T* __restrict__ dx, int acc) {
-  const int64_t nvec = rows * c / V;
-  const int cv = c / V;
+__global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
+    int64_t rows, int32_t c, int groups, int lanes, int64_t rows_per_block,
+    const T* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ relu_out,
+    const float* __restrict__ gamma, const float* __restrict__ mu,
+    const float* __restrict__ istd, const float* __restrict__ gsum, int batch_stat,
+    T* __restrict__ dx, int acc, float* __restrict__ bias_part) {
+  __shared__ float red[kBnThreads * 8];
+  const int g = threadIdx.x % groups, lane = threadIdx.x / groups;
+  const int c0 = (blockIdx.y * groups + g) * V;
+  const bool active = lane < lanes && c0 < c;
   const float fn = (float)rows;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % cv) * V;
-    float xv[V], gv[V], pv[V];
-    VecLoad<T, V>::load(x + i * V, xv);
-    VecLoad<T, V>::load(dy + i * V, gv);
-    if (relu_out) {
-      float zv[V];
-      VecLoad<T, V>::load(relu_out + i * V, zv);
+  float m[V], is[V], gg[V], gn[V], gb[V], gy2[V], cs[V];
 #pragma unroll
-      for (int j = 0; j < V; ++j) gv[j] = __fmul_rn(gv[j], zv[j] > 0.f ? 1.f : 0.f);
+  for (int j = 0; j < V; ++j) {
+    cs[j] = 0.f;
+    if (active) {
+      m[j] = mu[c0 + j];
+      is[j] = istd[c0 + j];
+      gg[j] = __fmul_rn(gamma[c0 + j], is[j]);   // g = gamma * istd
+      gn[j] = __fdiv_rn(gg[j], fn);              // g / n
+      gb[j] = gsum[c0 + j];                      // gbeta
+      gy2[j] = gsum[c + c0 + j];                 // ggamma
     }
-    if (acc) VecLoad<T, V>::load(dx + i * V, pv);
-    T out[V];
+  }
+  if (active) {
+    const int64_t r0 = blockIdx.x * rows_per_block;
+    const int64_t r1 = min(r0 + rows_per_block, rows);
+    for (int64_t rb = r0 + lane; rb < r1; rb += (int64_t)lanes * kUnroll) {
+      float xv[kUnroll][V], gv[kUnroll][V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int ch = c0 + j;
-      float g = __fmul_rn(gamma[ch], istd[ch]);
-      float r;
-      if (batch_stat) {
-        float xh = __fmul_rn(__fsub_rn(xv[j], mu[ch]), istd[ch]);
-        float t = __fsub_rn(__fmul_rn(fn, gv[j]), gsum[ch]);
-        t = __fsub_rn(t, __fmul_rn(xh, gsum[c + ch]));
-        r = __fmul_rn(__fdiv_rn(g, fn), t);
-      } else {
-        r = __fmul_rn(g, gv[j]);
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t r = rb + (int64_t)u * lanes;
+        if (r < r1) {
+          VecLoad<T, V>::load(dy + r * c + c0, gv[u]);
+          if (batch_stat) VecLoad<T, V>::load(x + r * c + c0, xv[u]);
+          if (relu_out) {
+            float zv[V];
+            VecLoad<T, V>::load(relu_out + r * c + c0, zv);
+#pragma unroll
+            for (int j = 0; j < V; ++j) gv[u][j] = __fmul_rn(gv[u][j], zv[j] > 0.f ? 1.f : 0.f);
+          }
+        }
       }
-      out[j] = Elem<T>::st(__fadd_rn(acc ? pv[j] : 0.f, r));
-    }
-    if (V == 8 && sizeof(T) == 2) {
-      *reinterpret_cast<uint4*>(dx + i * V) = *reinterpret_cast<uint4*>(out);
-    } else {
 #pragma unroll
-      for (int j = 0; j < V; ++j) dx[i * V + j] = out[j];
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t r = rb + (int64_t)u * lanes;
+        if (r >= r1) break;
+        float pv[V];
+        if (acc) VecLoad<T, V>::load(dx + r * c + c0, pv);
+        T out[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          float res;
+          if (batch_stat) {
+            const float xh = __fmul_rn(__fsub_rn(xv[u][j], m[j]), is[j]);
+            float t = __fsub_rn(__fmul_rn(fn, gv[u][j]), gb[j]);
+            t = __fsub_rn(t, __fmul_rn(xh, gy2[j]));
+            res = __fmul_rn(gn[j], t);
+          } else {
+            res = __fmul_rn(gg[j], gv[u][j]);
+          }
+          out[j] = Elem<T>::st(__fadd_rn(acc ? pv[j] : 0.f, res));
+          cs[j] += Elem<T>::ld(out[j]);
+        }
+        VecStore<T, V>::store(dx + r * c + c0, out);
+      }
     }
+  }
+  if (!bias_part) return;
+  const int width = groups * V;
+  if (lane < lanes) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[lane * width + g * V + j] = cs[j];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < width; col += kBnThreads) {
+    const int ch = blockIdx.y * groups * V + col;
+    if (ch >= c) continue;
+    float a = 0.f;
+    for (int l = 0; l < lanes; ++l) a += red[l * width + col];
+    float* out = bias_part + (int64_t)blockIdx.x * 2 * c;
+    out[ch] = a;
+    out[c + ch] = 0.f;
+  }
+}
+
+// db = q(prev + sum of bias partials) (fixed-order f64 reduction)
+template <typename T>
+__global__ void __launch_bounds__(1024) k_bn_bias_finalize(const float* __restrict__ partials,
+                                                           int32_t R, int32_t c, T* __restrict__ db,
+                                                           int acc, int32_t* __restrict__ nonfinite) {
+  const int ch = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s1, s2;
+  reduce_partials(partials, R, c, ch, s1, s2);
+  if ((threadIdx.x >> 5) == 0 && ch < c) {
+    write_out(db + ch, (float)s1, acc != 0);
+    if (nonfinite && !isfinite(Elem<T>::load(db + ch))) atomicOr(nonfinite, 1);
   }
 }
 
@@ -333,7 +428,7 @@ static size_t bn_ws_bytes(int64_t rows, int32_t c) {
   BnGeom g1 = bn_geom(c, false);
   int64_t bx1 = bn_blocks_x(rows, g1);
   if (bx1 > bx) bx = bx1;
-  return (size_t)(bx * 2 * c + 2 * c) * sizeof(float) + 256;
+  return (size_t)(2 * bx * 2 * c + 2 * c) * sizeof(float) + 256;
 }
 
 template <typename T, int MODE>
@@ -362,19 +457,42 @@ extern "C" {
 
 size_t nnl_bn_workspace_size(int64_t rows, int32_t c) { return bn_ws_bytes(rows, c); }
 
+}  // extern "C"
+
+template <typename T>
+static int launch_fwd_apply(int64_t rows, int32_t c, const BnGeom& g, const T* x,
+                            const float* gamma, const float* beta, const float* mu,
+                            const float* istd, T* y, int fuse_relu, cudaStream_t st) {
+  int64_t bx = bn_blocks_x(rows, g);
+  int64_t rpb = (rows + bx - 1) / bx;
+  dim3 grid((unsigned)bx, (unsigned)g.slabs);
+  if (g.vec == 8)
+    k_bn_fwd_apply<T, 8><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, gamma,
+                                                      beta, mu, istd, y, fuse_relu);
+  else
+    k_bn_fwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, gamma,
+                                                      beta, mu, istd, y, fuse_relu);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+extern "C" {
+
 int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const float* gamma,
                      const float* beta, float* running_mean, float* running_var, float eps,
                      float momentum, const float* stat_partials, int32_t n_partials,
                      float* save_mean, float* save_istd, void* y, int fuse_relu, void* ws,
                      size_t ws_bytes, void* stream) {
-  if (rows <= 1) return fail(NNL_ERR_DEGENERATE_BATCH, "cannot take batch statistics over %lld element(s)", (long long)rows);
+  if (rows <= 1)
+    return fail(NNL_ERR_DEGENERATE_BATCH, "cannot take batch statistics over %lld element(s)",
+                (long long)rows);
   cudaStream_t st = as_stream(stream);
-  bool vec = al16(x) && al16(y);
-  BnGeom g = bn_geom(c, vec);
+  BnGeom g = bn_geom(c, al16(x) && al16(y));
   const float* parts = stat_partials;
   int32_t R = n_partials;
   if (!parts) {
-    if (ws_bytes < bn_ws_bytes(rows, c)) return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
+    if (ws_bytes < bn_ws_bytes(rows, c))
+      return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
     int64_t bx = bn_blocks_x(rows, g);
     float* p = (float*)ws;
     int rc;
@@ -389,17 +507,12 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
   k_bn_finalize_fwd<<<(c + 31) / 32, 1024, 0, st>>>(parts, R, c, rows, running_mean, running_var,
                                                    eps, momentum, save_mean, save_istd);
   NNL_CHECK_LAUNCH();
-  int64_t nvec = rows * c / g.vec;
+  int rc;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    if (g.vec == 8)
-      k_bn_fwd_apply<T, 8><<<grid_for(nvec, 256, 148 * 32), 256, 0, st>>>(
-          rows, c, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y, fuse_relu);
-    else
-      k_bn_fwd_apply<T, 1><<<grid_for(nvec, 256, 148 * 32), 256, 0, st>>>(
-          rows, c, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y, fuse_relu);
+    rc = launch_fwd_apply<T>(rows, c, g, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y,
+                             fuse_relu, st);
   });
-  NNL_CHECK_LAUNCH();
-  return NNL_OK;
+  return rc;
 }
 
 int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x, const float* gamma,
@@ -409,33 +522,28 @@ int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x, const flo
   k_bn_eval_stats<<<(c + 255) / 256, 256, 0, st>>>(c, mean, var, eps, save_mean, save_istd);
   NNL_CHECK_LAUNCH();
   if (rows * c <= 0) return NNL_OK;
-  bool vec = al16(x) && al16(y) && c % 8 == 0;
-  int V = vec ? 8 : 1;
-  int64_t nvec = rows * c / V;
+  BnGeom g = bn_geom(c, al16(x) && al16(y));
+  int rc;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    if (V == 8)
-      k_bn_fwd_apply<T, 8><<<grid_for(nvec, 256, 148 * 32), 256, 0, st>>>(
-          rows, c, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y, fuse_relu);
-    else
-      k_bn_fwd_apply<T, 1><<<grid_for(nvec, 256, 148 * 32), 256, 0, st>>>(
-          rows, c, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y, fuse_relu);
+    rc = launch_fwd_apply<T>(rows, c, g, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y,
+                             fuse_relu, st);
   });
-  NNL_CHECK_LAUNCH();
-  return NNL_OK;
+  return rc;
 }
 
 int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy,
                const void* relu_out, const float* gamma, const float* save_mean,
                const float* save_istd, int batch_stat, void* dx, int acc_x, float* dgamma,
-               int acc_g, float* dbeta, int acc_b, int32_t* nonfinite, void* ws, size_t ws_bytes,
-               void* stream) {
+               int acc_g, float* dbeta, int acc_b, void* conv_bias_grad, int acc_cb,
+               int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
-  if (ws_bytes < bn_ws_bytes(rows, c)) return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
-  bool vec = al16(x) && al16(dy) && al16(relu_out) && al16(dx);
-  BnGeom g = bn_geom(c, vec);
+  if (ws_bytes < bn_ws_bytes(rows, c))
+    return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
+  BnGeom g = bn_geom(c, al16(x) && al16(dy) && al16(relu_out) && al16(dx));
   int64_t bx = bn_blocks_x(rows, g);
   float* parts = (float*)ws;
   float* gsum = parts + bx * 2 * c;
+  float* bparts = gsum + 2 * c;
   int rc;
   NNL_DISPATCH_DTYPE(dtype, T, {
     rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, (const T*)relu_out,
@@ -446,18 +554,25 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
                                                    dbeta, acc_b, nonfinite);
   NNL_CHECK_LAUNCH();
   if (!dx) return NNL_OK;
-  int64_t nvec = rows * c / g.vec;
+  const int64_t rpb = (rows + bx - 1) / bx;
+  dim3 grid((unsigned)bx, (unsigned)g.slabs);
+  float* bp = conv_bias_grad ? bparts : nullptr;
   NNL_DISPATCH_DTYPE(dtype, T, {
     if (g.vec == 8)
-      k_bn_bwd_apply<T, 8><<<grid_for(nvec, 256, 148 * 32), 256, 0, st>>>(
-          rows, c, (const T*)x, (const T*)dy, (const T*)relu_out, gamma, save_mean, save_istd,
-          gsum, batch_stat, (T*)dx, acc_x);
+      k_bn_bwd_apply<T, 8><<<grid, kBnThreads, 0, st>>>(
+          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, (const T*)relu_out, gamma,
+          save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
     else
-      k_bn_bwd_apply<T, 1><<<grid_for(nvec, 256, 148 * 32), 256, 0, st>>>(
-          rows, c, (const T*)x, (const T*)dy, (const T*)relu_out, gamma, save_mean, save_istd,
-          gsum, batch_stat, (T*)dx, acc_x);
+      k_bn_bwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(
+          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, (const T*)relu_out, gamma,
+          save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
+    NNL_CHECK_LAUNCH();
+    if (bp) {
+      k_bn_bias_finalize<T><<<(c + 31) / 32, 1024, 0, st>>>(bp, (int32_t)bx, c,
+                                                            (T*)conv_bias_grad, acc_cb, nonfinite);
+      NNL_CHECK_LAUNCH();
+    }
   });
-  NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
 

@@ -236,12 +236,13 @@ __global__ void k_gap_bwd(int64_t n, int64_t hw, int64_t c, const T* __restrict_
 template <typename T>
 __global__ void k_import(int32_t n, int32_t c, int32_t hw, const float* __restrict__ src,
                          T* __restrict__ dst) {
-  int64_t total = (int64_t)n * c * hw;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t ch = i % c;
-    int64_t pix = (i / c) % hw;
-    int64_t b = i / ((int64_t)c * hw);
+  // 32-bit index math (the host guarantees n*c*hw < 2^31)
+  const int total = n * c * hw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int ch = i % c;
+    const int rest = i / c;
+    const int pix = rest % hw;
+    const int b = rest / hw;
     Elem<T>::store(dst + i, src[(b * c + ch) * hw + pix]);
   }
 }
@@ -249,12 +250,12 @@ __global__ void k_import(int32_t n, int32_t c, int32_t hw, const float* __restri
 template <typename T>
 __global__ void k_export(int32_t n, int32_t c, int32_t hw, const T* __restrict__ src,
                          float* __restrict__ dst) {
-  int64_t total = (int64_t)n * c * hw;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t pix = i % hw;
-    int64_t ch = (i / hw) % c;
-    int64_t b = i / ((int64_t)c * hw);
+  const int total = n * c * hw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int pix = i % hw;
+    const int rest = i / hw;
+    const int ch = rest % c;
+    const int b = rest / c;
     dst[i] = Elem<T>::load(src + (b * hw + pix) * c + ch);
   }
 }
@@ -422,6 +423,7 @@ int nnl_import_f32(int dtype, int32_t n, int32_t c, int32_t hw, const float* src
                    void* stream) {
   int64_t total = (int64_t)n * c * hw;
   if (total <= 0) return NNL_OK;
+  if (total >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "import of >= 2^31 elements");
   NNL_DISPATCH_DTYPE(dtype, T, {
     k_import<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(n, c, hw, src, (T*)dst);
   });
@@ -433,6 +435,7 @@ int nnl_export_f32(int dtype, int32_t n, int32_t c, int32_t hw, const void* src,
                    void* stream) {
   int64_t total = (int64_t)n * c * hw;
   if (total <= 0) return NNL_OK;
+  if (total >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "export of >= 2^31 elements");
   NNL_DISPATCH_DTYPE(dtype, T, {
     k_export<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(n, c, hw, (const T*)src, dst);
   });

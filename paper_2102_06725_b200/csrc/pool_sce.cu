@@ -88,6 +88,109 @@ __global__ void k_maxpool_bwd(nnl_pool_shape ps, const T* __restrict__ dy,
   }
 }
 
+// Vectorised variants (fp16, C % 8 == 0, < 2^31 elements): one thread owns 8
+// channels of one pixel, 32-bit index math, 16-byte loads/stores.  Same
+// semantics as the scalar kernels above.
+__global__ void k_maxpool_fwd_h8(nnl_pool_shape ps, const uint4* __restrict__ x,
+                                 uint4* __restrict__ y, uint2* __restrict__ arg) {
+  const int cg = ps.c >> 3;
+  const int total = ps.n * ps.p * ps.q * cg;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % cg;
+    int t = i / cg;
+    const int oq = t % ps.q;
+    t /= ps.q;
+    const int op = t % ps.p;
+    const int b = t / ps.p;
+    float best[8];
+    uint8_t bi[8];
+    bool nan[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { best[j] = -INFINITY; bi[j] = 0; nan[j] = false; }
+    for (int di = 0; di < ps.kh; ++di) {
+      const int ih = op * ps.sh - ps.ph + di;
+      for (int dj = 0; dj < ps.kw; ++dj) {
+        const int iw = oq * ps.sw - ps.pw + dj;
+        const int idx = di * ps.kw + dj;
+        float v[8];
+        if (ih >= 0 && ih < ps.h && iw >= 0 && iw < ps.w) {
+          uint4 u = x[((b * ps.h + ih) * ps.w + iw) * cg + g];
+          const __half* h = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = __half2float(h[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (nan[j]) continue;
+          if (v[j] != v[j]) {
+            nan[j] = true; best[j] = v[j]; bi[j] = (uint8_t)idx;
+          } else if (idx == 0 || v[j] > best[j]) {
+            best[j] = v[j]; bi[j] = (uint8_t)idx;
+          }
+        }
+      }
+    }
+    uint4 o;
+    __half* oh = reinterpret_cast<__half*>(&o);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) oh[j] = __float2half_rn(best[j]);
+    y[i] = o;
+    uint2 a;
+    a.x = bi[0] | (bi[1] << 8) | (bi[2] << 16) | ((uint32_t)bi[3] << 24);
+    a.y = bi[4] | (bi[5] << 8) | (bi[6] << 16) | ((uint32_t)bi[7] << 24);
+    arg[i] = a;
+  }
+}
+
+__global__ void k_maxpool_bwd_h8(nnl_pool_shape ps, const uint4* __restrict__ dy,
+                                 const uint2* __restrict__ arg, uint4* __restrict__ dx, int acc) {
+  const int cg = ps.c >> 3;
+  const int total = ps.n * ps.h * ps.w * cg;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % cg;
+    int t = i / cg;
+    const int iw = t % ps.w;
+    t /= ps.w;
+    const int ih = t % ps.h;
+    const int b = t / ps.h;
+    const int hp = ih + ps.ph, wp = iw + ps.pw;
+    int p_lo = hp - ps.kh + 1;
+    p_lo = p_lo <= 0 ? 0 : (p_lo + ps.sh - 1) / ps.sh;
+    const int p_hi = min(hp / ps.sh, ps.p - 1);
+    int q_lo = wp - ps.kw + 1;
+    q_lo = q_lo <= 0 ? 0 : (q_lo + ps.sw - 1) / ps.sw;
+    const int q_hi = min(wp / ps.sw, ps.q - 1);
+    float s[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] = 0.f;
+    for (int op = p_lo; op <= p_hi; ++op) {
+      const int di = hp - op * ps.sh;
+      for (int oq = q_lo; oq <= q_hi; ++oq) {
+        const int want = di * ps.kw + (wp - oq * ps.sw);
+        const int o = ((b * ps.p + op) * ps.q + oq) * cg + g;
+        const uint2 a = arg[o];
+        const uint4 u = dy[o];
+        const __half* h = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t word = j < 4 ? a.x : a.y;
+          const int id = (word >> (8 * (j & 3))) & 0xff;
+          if (id == want) s[j] = __fadd_rn(s[j], __half2float(h[j]));
+        }
+      }
+    }
+    uint4 prev = acc ? dx[i] : make_uint4(0, 0, 0, 0);
+    __half* ph = reinterpret_cast<__half*>(&prev);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      ph[j] = __float2half_rn(__fadd_rn(acc ? __half2float(ph[j]) : 0.f, s[j]));
+    dx[i] = prev;
+  }
+}
+
 // ---- SoftmaxCrossEntropy ----------------------------------------------------
 // One warp per row.  row_stats[3*b] = (max, log-sum-exp, log p[label]).
 template <typename T>
@@ -168,6 +271,14 @@ int nnl_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x, void* y,
   if (ps->kh * ps->kw > 255) return fail(NNL_ERR_UNSUPPORTED, "pool window > 255 elements");
   int64_t total = (int64_t)ps->n * ps->p * ps->q * ps->c;
   if (total <= 0) return NNL_OK;
+  if (dtype == NNL_F16 && ps->c % 8 == 0 && (int64_t)ps->n * ps->h * ps->w * ps->c < (1ll << 31) &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+        reinterpret_cast<uintptr_t>(argmax)) & 15) == 0) {
+    k_maxpool_fwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+        *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
+    NNL_CHECK_LAUNCH();
+    return NNL_OK;
+  }
   NNL_DISPATCH_DTYPE(dtype, T, {
     k_maxpool_fwd<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(*ps, (const T*)x,
                                                                           (T*)y, argmax);
@@ -181,6 +292,14 @@ int nnl_maxpool_bwd(int dtype, const nnl_pool_shape* ps, const void* dy, const u
   if (!ps) return fail(NNL_ERR_INVALID_ARGUMENT, "null pool shape");
   int64_t total = (int64_t)ps->n * ps->h * ps->w * ps->c;
   if (total <= 0) return NNL_OK;
+  if (dtype == NNL_F16 && ps->c % 8 == 0 && total < (1ll << 31) &&
+      ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) |
+        reinterpret_cast<uintptr_t>(argmax)) & 15) == 0) {
+    k_maxpool_bwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+        *ps, (const uint4*)dy, (const uint2*)argmax, (uint4*)dx, accumulate);
+    NNL_CHECK_LAUNCH();
+    return NNL_OK;
+  }
   NNL_DISPATCH_DTYPE(dtype, T, {
     k_maxpool_bwd<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
         *ps, (const T*)dy, argmax, (T*)dx, accumulate);

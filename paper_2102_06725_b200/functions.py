@@ -222,11 +222,13 @@ class Convolution(FunctionImpl):
             ws = _lib.workspace(_lib.lib().nnl_conv2d_workspace_size(C.byref(cs), x.code, 1))
             _lib.call("nnl_conv2d_bwd_data", C.byref(cs), x.code, gy.ptr, w.ptr, gxs[0].ptr,
                       _flag(acc[0]), ws[0], ws[1], _st())
-        if gxs[1] is not None or gxs[2] is not None:
+        # the bias gradient was already reduced by the following BN's backward
+        gb = None if node.state.get("bias_by_bn") else gxs[2]
+        if gxs[1] is not None or gb is not None:
             ws = _lib.workspace(_lib.lib().nnl_conv2d_workspace_size(C.byref(cs), x.code, 2))
             _lib.call("nnl_conv2d_bwd_weight", C.byref(cs), x.code, x.ptr, gy.ptr,
                       gxs[1].ptr if gxs[1] is not None else None, _flag(acc[1]),
-                      gxs[2].ptr if gxs[2] is not None else None, _flag(acc[2]),
+                      gb.ptr if gb is not None else None, _flag(acc[2]),
                       node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
 
     def backward_reads_input(self, index):
@@ -431,13 +433,17 @@ class BatchNormalization(FunctionImpl):
         c = x.shape[1]
         rows = self._rows(x)
         ws = _lib.workspace(_lib.lib().nnl_bn_workspace_size(rows, c))
+        conv = node.inputs[0].parent
+        cbias = None
+        if gxs[0] is not None and conv is not None and conv.state.get("bias_by_bn"):
+            cbias = conv.inputs[2].grad.ptr  # sole consumer: first contribution overwrites
         _lib.call("nnl_bn_bwd", x.code, rows, c, x.ptr, gy.ptr, relu_out, gamma.ptr,
                   node.state["mean"].data_ptr(), node.state["istd"].data_ptr(),
                   1 if self.batch_stat else 0,
                   gxs[0].ptr if gxs[0] is not None else None, _flag(acc[0]),
                   gxs[1].ptr if gxs[1] is not None else None, _flag(acc[1]),
                   gxs[2].ptr if gxs[2] is not None else None, _flag(acc[2]),
-                  node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
+                  cbias, 0, node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
 
     def backward(self, node, gys, gxs, acc):
         self._backward(node, gys[0], None, gxs, acc)

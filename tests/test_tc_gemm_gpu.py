@@ -17,7 +17,40 @@ CONV = [  # (B, cin, cout, k, stride, pad, hw)
     (2, 64, 256, 1, 2, 0, 10),     # 1x1 s2 (downsample)
     (2, 3, 64, 7, 2, 3, 20),       # stem: explicit im2col
     (4, 256, 64, 1, 1, 0, 7),      # 1x1 reduce, 7x7 maps
+    (8, 256, 512, 1, 1, 0, 14),    # 256-wide tiles
+    (4, 256, 512, 1, 2, 0, 14),    # 1x1 s2 dgrad: row remap + zero fill
+    (16, 128, 256, 3, 1, 1, 14),   # 3x3 gather with 256-wide tiles
+    (64, 64, 128, 3, 1, 1, 20),    # > 148 work units: persistent tile loop
 ]
+
+
+def test_conv_backward_accumulate_mode(nnl):
+    """acc=True writes q(prev + grad) (R2) on every tcgen05 path."""
+    import paper_2102_06725_b200.functions as F
+    _half(nnl)
+    for geom in [(2, 64, 128, 1, 2, 0, 8), (2, 64, 64, 3, 1, 1, 8), (2, 128, 256, 1, 1, 0, 6)]:
+        b, cin, cout, k, s, p, hw = geom
+        rng = np.random.default_rng(k + cout)
+        x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+        w = rng.uniform(-0.2, 0.2, (cout, cin, k, k)).astype(np.float32)
+        bias = np.zeros(cout, np.float32)
+        vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+        for v, a in zip(vs, (x, w, bias)):
+            v.d = a
+        y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+        y.forward()
+        gy = O.q16(rng.uniform(-1, 1, y.shape).astype(np.float32))
+        y.g = gy
+        prev = [O.q16(rng.uniform(-1, 1, a.shape).astype(np.float32)) for a in (x, w, bias)]
+        for v, pv in zip(vs, prev):
+            v.g = pv
+        node = y.parent
+        node.impl.backward(node, [y.grad], [v.grad for v in vs], [True] * 3)
+        ov = [O.Var(a, half=True, need_grad=True) for a in (x, w, bias)]
+        oy = O.conv2d(*ov, (s, s), (p, p), True)
+        gxs = oy.parent.bwd([gy], [True, True, True])
+        for v, pv, want in zip(vs, prev, gxs):
+            assert _rel_err(v.g, O.q16(pv + want)) < 4e-3, geom
 
 
 def _half(nn):
