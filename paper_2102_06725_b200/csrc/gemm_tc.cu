@@ -30,8 +30,10 @@
 namespace nnl {
 using namespace tc;
 
-enum AMode { A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3 };
-enum BMode { B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2 };
+// A_IM2COL / B_IM2COL: TMA im2col mode (fprop + stride-1 dgrad A, wgrad B);
+// the cp.async gathers remain for strided dgrad and as a debug path.
+enum AMode { A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4 };
+enum BMode { B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3 };
 
 constexpr int BM = 128, BK = 64, kThreads = 384;
 
@@ -43,7 +45,8 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int PIPE = STAGES * (A_BYTES + B_BYTES);
   static constexpr int RED_BYTES = 4 * BN * 2 * 4;
-  static constexpr int SMEM = PIPE + 1024 + RED_BYTES + 1024;
+  static constexpr int BIAS_BYTES = BN * 4;
+  static constexpr int SMEM = PIPE + 1024 + RED_BYTES + BIAS_BYTES + 1024;
 };
 
 struct TcArgs {
@@ -59,6 +62,10 @@ struct TcArgs {
   int64_t ldc;
   int acc;
   int remap;          // output row m=(n,p,q) -> (n, p*sh, q*sw) of an H x W map
+  // im2col TMA: GEMM rows (A) / reduction rows (B) enumerate an (gh x gw)
+  // pixel grid per image; pixel (y, x) has window base (y*ish + ilh, x*isw + ilw)
+  int gh, gw, ish, isw, ilh, ilw;
+  int flip;           // dgrad: tap t of the im2col load uses weight tap R*S-1-t
   const __half* bias;
   float* stats;
   int32_t* nonfinite;
@@ -87,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const TcArgs a) {
   using C = Cfg<BN>;
   constexpr int S = C::STAGES;
-  constexpr bool kGA = AM >= A_GATHER_FPROP;
+  constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD;
   constexpr bool kGB = BMD == B_GATHER_WGRAD;
   constexpr bool kAmn = AM == A_TMA_MN;
   constexpr bool kBmn = BMD != B_TMA_K;
@@ -105,6 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* red = reinterpret_cast<float*>(smem + C::PIPE + 1024);
+  float* bias_s = reinterpret_cast<float*>(smem + C::PIPE + 1024 + C::RED_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ConvGeom& g = a.g;
@@ -137,13 +145,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         const Unit w = decode_unit(a, u);
         const int m0 = w.tm * BM, n0 = w.tn * BN;
+        // im2col A: window base of the tile's first row pixel
+        int a_x = 0, a_y = 0, a_n = 0;
+        if (AM == A_IM2COL) {
+          a_x = m0 % a.gw;
+          const int t = m0 / a.gw;
+          a_y = t % a.gh;
+          a_n = t / a.gh;
+        }
         for (int i = 0; i < w.nk; ++i, ++it) {
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           const int kb = w.kb0 + i;
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_tx(&full[s], kTmaBytes);
-          if (AM == A_TMA_K) {
+          if (AM == A_IM2COL) {
+            const int t = kb / a.cblk, cb = kb - t * a.cblk;
+            const int r = t / g.s, sx = t - r * g.s;
+            tma_load_im2col(stA + s * C::A_BYTES, &tmA, &full[s], cb * 64, a_x * a.isw + a.ilw,
+                            a_y * a.ish + a.ilh, a_n, (uint16_t)sx, (uint16_t)r);
+          } else if (AM == A_TMA_K) {
             tma_load_2d(stA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
           } else if (AM == A_TMA_MN) {
 #pragma unroll
@@ -153,11 +174,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (BMD == B_TMA_K) {
             tma_load_2d(stB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
           } else if (BMD == B_TMA_MN) {
-            const int t = kb / a.b_kblk, kob = kb - t * a.b_kblk;
+            int t = kb / a.b_kblk;
+            const int kob = kb - t * a.b_kblk;
+            if (a.flip) t = g.r * g.s - 1 - t;
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
               tma_load_2d(stB + s * C::B_BYTES + j * 8192, &tmB, &full[s],
                           t * a.b_tap_stride + n0 + 64 * j, kob * BK);
+          } else if (BMD == B_IM2COL) {
+            // 64 reduction pixels x 64 channels of tap (r, s) per 64-wide N block
+            const int pix0 = kb * BK;
+            const int bx = pix0 % a.gw, t0 = pix0 / a.gw;
+            const int by = t0 % a.gh, bn_ = t0 / a.gh;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              const int cbg = (n0 >> 6) + j;
+              const int t = cbg / a.cblk, cb = cbg - t * a.cblk;
+              const int r = t / g.s, sx = t - r * g.s;
+              tma_load_im2col(stB + s * C::B_BYTES + j * 8192, &tmB, &full[s], cb * 64,
+                              bx * a.isw + a.ilw, by * a.ish + a.ilh, bn_, (uint16_t)sx,
+                              (uint16_t)r);
+            }
           }
         }
       }
@@ -334,6 +371,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit w = decode_unit(a, u);
       const int m0 = w.tm * BM, n0 = w.tn * BN;
       const int ab = t & 1;
+      if (a.bias) {  // this tile's bias slice, staged once in shared memory (as f32)
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        for (int j = tid; j < BN; j += 128)
+          bias_s[j] = n0 + j < a.N ? __half2float(a.bias[n0 + j]) : 0.f;
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      }
       mbar_wait(&tfull[ab], (t >> 1) & 1);
       tc_fence_after();
       const int row = wq * 32 + lane;
@@ -372,8 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
         if (a.bias) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (nb + j < a.N) f[j] = __fadd_rn(f[j], __half2float(a.bias[nb + j]));
+          for (int j = 0; j < 32; ++j) f[j] = __fadd_rn(f[j], bias_s[c + j]);
         }
         __half* dsth = reinterpret_cast<__half*>(a.out) + orow * a.ldc + nb;
         __align__(16) __half hv[32];
@@ -573,6 +615,60 @@ struct View {  // a row-major fp16 matrix [rows][cols] with a row stride
   int64_t rows = 0, cols = 0, ld = 0;
 };
 
+// im2col-mode TMA view of an NHWC tensor (dims C, W, H, N innermost first)
+struct Im2colView {
+  const void* ptr = nullptr;
+  int c = 0, w = 0, h = 0, n = 0;
+  int lw = 0, lh = 0, uw = 0, uh = 0;  // bounding-box corners of the window bases
+  int sw = 1, sh = 1;                  // traversal strides
+  int pixels = 0;                      // pixels per load (tile rows)
+};
+
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                   cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  }
+  return fn;
+}
+
+static int make_im2col_tmap(CUtensorMap* tm, const Im2colView& v) {
+  EncodeIm2colFn enc = encode_im2col_fn();
+  if (!enc) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
+  if (reinterpret_cast<uintptr_t>(v.ptr) & 15) return fail(NNL_ERR_UNSUPPORTED, "im2col base");
+  cuuint64_t dims[4] = {(cuuint64_t)v.c, (cuuint64_t)v.w, (cuuint64_t)v.h, (cuuint64_t)v.n};
+  cuuint64_t strides[3] = {(cuuint64_t)v.c * 2, (cuuint64_t)v.w * v.c * 2,
+                           (cuuint64_t)v.h * v.w * v.c * 2};
+  int lower[2] = {v.lw, v.lh}, upper[2] = {v.uw, v.uh};
+  cuuint32_t es[4] = {1, (cuuint32_t)v.sw, (cuuint32_t)v.sh, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(v.ptr), dims, strides,
+                   lower, upper, 64, (cuuint32_t)v.pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
+  return NNL_OK;
+}
+
+static bool use_tma_im2col() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NNL_TC_GATHER");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int make_tmap(CUtensorMap* tm, const View& v, int box_cols, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -598,6 +694,8 @@ struct Plan {
   int kp = 0;            // padded reduction width of the im2col matrix
   bool pad_w = false;    // fprop im2col: weights padded to [k][kp]
   bool remap = false;    // 1x1 strided dgrad: rows scatter to (n, p*sh, q*sw)
+  Im2colView im;         // A_IM2COL / B_IM2COL source
+  int gh = 0, gw = 0, ish = 1, isw = 1, ilh = 0, ilw = 0, flip = 0;
   int cblk = 0, b_kblk = 0, b_tap_stride = 0;
   const void* gsrc = nullptr;
   int64_t ldc = 0;
@@ -661,6 +759,11 @@ static Plan make_plan(const GemmProblem& pb) {
       pl.bmode = B_TMA_K; pl.B = {pb.b, g.k, rsc, rsc};
       if (one) {
         pl.amode = A_TMA_K; pl.A = {pb.a, nhw, g.c, g.c};
+      } else if (use_tma_im2col()) {
+        pl.amode = A_IM2COL; pl.cblk = g.c / 64;
+        pl.im = {pb.a, g.c, g.w, g.h, g.n, -g.pw, -g.ph, g.pw - (g.s - 1), g.ph - (g.r - 1),
+                 g.sw, g.sh, BM};
+        pl.gh = g.p; pl.gw = g.q; pl.ish = g.sh; pl.isw = g.sw; pl.ilh = -g.ph; pl.ilw = -g.pw;
       } else {
         pl.amode = A_GATHER_FPROP; pl.gsrc = pb.a; pl.cblk = g.c / 64;
       }
@@ -684,6 +787,14 @@ static Plan make_plan(const GemmProblem& pb) {
       pl.M = (int)npq;
       pl.amode = A_TMA_K; pl.A = {pb.a, npq, g.k, g.k};
       pl.remap = !one;
+    } else if (g.sh == 1 && g.sw == 1 && use_tma_im2col()) {
+      // stride-1 dgrad is a convolution of dy with the flipped filter:
+      // dx(y,x) = sum_{r',s'} dy(y + ph-(R-1) + r', x + pw-(S-1) + s') W[R-1-r'][S-1-s']
+      pl.M = (int)nhw;
+      pl.amode = A_IM2COL; pl.cblk = g.k / 64; pl.flip = 1;
+      const int lw = g.pw - (g.s - 1), lh = g.ph - (g.r - 1);
+      pl.im = {pb.a, g.k, g.q, g.p, g.n, lw, lh, lw + g.w - g.q, lh + g.h - g.p, 1, 1, BM};
+      pl.gh = g.h; pl.gw = g.w; pl.ish = 1; pl.isw = 1; pl.ilh = lh; pl.ilw = lw;
     } else {
       pl.M = (int)nhw;
       pl.amode = A_GATHER_DGRAD; pl.gsrc = pb.a; pl.cblk = g.k / 64;
@@ -695,6 +806,11 @@ static Plan make_plan(const GemmProblem& pb) {
     if (g.c % 64 == 0) {
       if (one) {
         pl.bmode = B_TMA_MN; pl.B = {pb.b, nhw, g.c, g.c};
+      } else if (use_tma_im2col()) {
+        pl.bmode = B_IM2COL; pl.cblk = g.c / 64;
+        pl.im = {pb.b, g.c, g.w, g.h, g.n, -g.pw, -g.ph, g.pw - (g.s - 1), g.ph - (g.r - 1),
+                 g.sw, g.sh, 64};
+        pl.gh = g.p; pl.gw = g.q; pl.ish = g.sh; pl.isw = g.sw; pl.ilh = -g.ph; pl.ilw = -g.pw;
       } else {
         pl.bmode = B_GATHER_WGRAD; pl.gsrc = pb.b; pl.cblk = g.c / 64;
       }
@@ -757,6 +873,9 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   NNL_TC_CASE(A_GATHER_FPROP, B_TMA_K)
   NNL_TC_CASE(A_GATHER_DGRAD, B_TMA_MN)
   NNL_TC_CASE(A_TMA_MN, B_GATHER_WGRAD)
+  NNL_TC_CASE(A_IM2COL, B_TMA_K)
+  NNL_TC_CASE(A_IM2COL, B_TMA_MN)
+  NNL_TC_CASE(A_TMA_MN, B_IM2COL)
 #undef NNL_TC_CASE
   return fail(NNL_ERR_UNSUPPORTED, "no tcgen05 kernel for mode %d/%d", pl.amode, pl.bmode);
 }
@@ -830,11 +949,15 @@ int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStr
     if ((rc = make_tmap(&ta, pl.A, 64, BM))) return rc;
   } else if (pl.amode == A_TMA_MN) {
     if ((rc = make_tmap(&ta, pl.A, 64, 64))) return rc;
+  } else if (pl.amode == A_IM2COL) {
+    if ((rc = make_im2col_tmap(&ta, pl.im))) return rc;
   }
   if (pl.bmode == B_TMA_K) {
     if ((rc = make_tmap(&tb, pl.B, 64, pl.bn))) return rc;
   } else if (pl.bmode == B_TMA_MN) {
     if ((rc = make_tmap(&tb, pl.B, 64, 64))) return rc;
+  } else if (pl.bmode == B_IM2COL) {
+    if ((rc = make_im2col_tmap(&tb, pl.im))) return rc;
   }
   TcArgs args;
   memset(&args, 0, sizeof(args));
@@ -844,6 +967,8 @@ int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStr
   args.gsrc = reinterpret_cast<const __half*>(pl.gsrc);
   args.cblk = pl.cblk; args.b_kblk = pl.b_kblk; args.b_tap_stride = pl.b_tap_stride;
   args.out = pb.out; args.ldc = pl.ldc; args.acc = pb.acc; args.remap = pl.remap;
+  args.gh = pl.gh; args.gw = pl.gw; args.ish = pl.ish; args.isw = pl.isw;
+  args.ilh = pl.ilh; args.ilw = pl.ilw; args.flip = pl.flip;
   args.bias = reinterpret_cast<const __half*>(pb.bias);
   args.stats = pb.stats; args.nonfinite = pb.nonfinite;
   args.partial = pl.splits > 1 ? partial : nullptr;

@@ -56,6 +56,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
       : "memory");
 }
 
+// im2col mode over a (C, W, H, N) tensor: `pixels` consecutive filter-window
+// base positions starting at (w, h, n), each shifted by the tap offset
+// (offw, offh), `channels` channels from c; padding reads as zero.
+__device__ __forceinline__ void tma_load_im2col(void* dst, const void* tmap, uint64_t* bar, int c,
+                                                int w, int h, int n, uint16_t offw,
+                                                uint16_t offh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(offw), "h"(offh)
+      : "memory");
+}
+
 // ---- cp.async gathers (16 B, zero-filled when src_bytes == 0) -------------------
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
