@@ -61,7 +61,12 @@ struct TcArgs {
   void* out;
   int64_t ldc;
   int acc;
-  int remap;          // output row m=(n,p,q) -> (n, p*sh, q*sw) of an H x W map
+  int remap;          // output row m=(n,y,x) of an (rgh x rgw) grid -> dx pixel
+  int rgh, rgw, rsh, rsw, ra, rb;  //   (n, y*rsh + ra, x*rsw + rb) of the H x W map
+  // strided-dgrad parity class: k-block tap t uses im2col offsets tap_offw/h[t]
+  // and weight tap tap_w[t] (ntap == 0: taps come from t = r*S + s)
+  int ntap;
+  uint8_t tap_w[16], tap_offw[16], tap_offh[16];
   // im2col TMA: GEMM rows (A) / reduction rows (B) enumerate an (gh x gw)
   // pixel grid per image; pixel (y, x) has window base (y*ish + ilh, x*isw + ilw)
   int gh, gw, ish, isw, ilh, ilw;
@@ -161,7 +166,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_tx(&full[s], kTmaBytes);
           if (AM == A_IM2COL) {
             const int t = kb / a.cblk, cb = kb - t * a.cblk;
-            const int r = t / g.s, sx = t - r * g.s;
+            int r, sx;
+            if (a.ntap) {
+              r = a.tap_offh[t];
+              sx = a.tap_offw[t];
+            } else {
+              r = t / g.s;
+              sx = t - r * g.s;
+            }
             tma_load_im2col(stA + s * C::A_BYTES, &tmA, &full[s], cb * 64, a_x * a.isw + a.ilw,
                             a_y * a.ish + a.ilh, a_n, (uint16_t)sx, (uint16_t)r);
           } else if (AM == A_TMA_K) {
@@ -176,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if (BMD == B_TMA_MN) {
             int t = kb / a.b_kblk;
             const int kob = kb - t * a.b_kblk;
-            if (a.flip) t = g.r * g.s - 1 - t;
+            if (a.ntap) t = a.tap_w[t];
+            else if (a.flip) t = g.r * g.s - 1 - t;
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
               tma_load_2d(stB + s * C::B_BYTES + j * 8192, &tmB, &full[s],
@@ -384,9 +397,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool mv = m < a.M;
       int64_t orow = m;
       if (a.remap && mv) {
-        const int q = m % g.q, tt = m / g.q;
-        const int p = tt % g.p, n = tt / g.p;
-        orow = ((int64_t)n * g.h + p * g.sh) * g.w + q * g.sw;
+        const int x = m % a.rgw, tt = m / a.rgw;
+        const int y = tt % a.rgh, n = tt / a.rgh;
+        orow = ((int64_t)n * g.h + y * a.rsh + a.ra) * g.w + x * a.rsw + a.rb;
       }
       int bad = 0;
       for (int c = 0; c < BN; c += 32) {
@@ -696,6 +709,10 @@ struct Plan {
   bool remap = false;    // 1x1 strided dgrad: rows scatter to (n, p*sh, q*sw)
   Im2colView im;         // A_IM2COL / B_IM2COL source
   int gh = 0, gw = 0, ish = 1, isw = 1, ilh = 0, ilw = 0, flip = 0;
+  int rgh = 0, rgw = 0, rsh = 1, rsw = 1, ra = 0, rb = 0;
+  int nclass = 0;        // strided dgrad: number of output parity classes
+  int ntap = 0;
+  uint8_t tap_w[16] = {}, tap_offw[16] = {}, tap_offh[16] = {};
   int cblk = 0, b_kblk = 0, b_tap_stride = 0;
   const void* gsrc = nullptr;
   int64_t ldc = 0;
@@ -725,7 +742,51 @@ static int pick_bn(const Plan& pl, bool tap_split_b) {
   return best;
 }
 
-static Plan make_plan(const GemmProblem& pb) {
+// Strided dgrad, output parity class (a, b): pixels (y*sh + a, x*sw + b) only
+// receive taps r = a+ph (mod sh), s = b+pw (mod sw), reading dy at
+// (y + (a+ph-r)/sh, x + (b+pw-s)/sw).  That is a stride-1 im2col GEMM over dy
+// with 1..ceil(R/sh)*ceil(S/sw) taps: 9 taps of work in total instead of the
+// 4x36 a zero-skipping-free gather would multiply.
+static bool strided_class(const ConvGeom& g, int cls, Plan& pl) {
+  const int a = cls / g.sw, b = cls % g.sw;
+  int tr[16], dr[16], ts[16], ds[16], nr = 0, ns = 0;
+  for (int r = 0; r < g.r && nr < 16; ++r) {
+    const int x = a + g.ph - r;
+    if (((x % g.sh) + g.sh) % g.sh == 0) { tr[nr] = r; dr[nr] = x / g.sh; ++nr; }
+  }
+  for (int s = 0; s < g.s && ns < 16; ++s) {
+    const int x = b + g.pw - s;
+    if (((x % g.sw) + g.sw) % g.sw == 0) { ts[ns] = s; ds[ns] = x / g.sw; ++ns; }
+  }
+  if (nr == 0 || ns == 0 || nr * ns > 16) return false;
+  int dmr = dr[0], dms = ds[0];
+  for (int i = 1; i < nr; ++i) dmr = dr[i] < dmr ? dr[i] : dmr;
+  for (int j = 1; j < ns; ++j) dms = ds[j] < dms ? ds[j] : dms;
+  pl.ntap = nr * ns;
+  for (int i = 0; i < nr; ++i)
+    for (int j = 0; j < ns; ++j) {
+      const int t = i * ns + j;
+      pl.tap_w[t] = (uint8_t)(tr[i] * g.s + ts[j]);
+      pl.tap_offh[t] = (uint8_t)(dr[i] - dmr);
+      pl.tap_offw[t] = (uint8_t)(ds[j] - dms);
+    }
+  const int gh = g.h > a ? (g.h - a + g.sh - 1) / g.sh : 0;
+  const int gw = g.w > b ? (g.w - b + g.sw - 1) / g.sw : 0;
+  pl.gh = gh; pl.gw = gw; pl.ish = 1; pl.isw = 1; pl.ilh = dmr; pl.ilw = dms;
+  pl.rgh = gh; pl.rgw = gw; pl.rsh = g.sh; pl.rsw = g.sw; pl.ra = a; pl.rb = b;
+  pl.remap = true;
+  return gh > 0 && gw > 0;
+}
+
+static bool strided_ok(const ConvGeom& g) {
+  for (int c = 0; c < g.sh * g.sw; ++c) {
+    Plan tmp;
+    if (!strided_class(g, c, tmp)) return false;
+  }
+  return g.sh * g.sw <= 16;
+}
+
+static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   Plan pl;
   const ConvGeom& g = pb.g;
   const bool k1 = g.r == 1 && g.s == 1 && g.ph == 0 && g.pw == 0;
@@ -787,6 +848,15 @@ static Plan make_plan(const GemmProblem& pb) {
       pl.M = (int)npq;
       pl.amode = A_TMA_K; pl.A = {pb.a, npq, g.k, g.k};
       pl.remap = !one;
+      pl.rgh = g.p; pl.rgw = g.q; pl.rsh = g.sh; pl.rsw = g.sw;
+    } else if ((g.sh > 1 || g.sw > 1) && use_tma_im2col() && strided_ok(g) &&
+               strided_class(g, cls, pl)) {
+      pl.nclass = g.sh * g.sw;
+      pl.M = (int)((int64_t)g.n * pl.gh * pl.gw);
+      pl.K = pl.ntap * g.k;
+      pl.amode = A_IM2COL; pl.cblk = g.k / 64;
+      pl.im = {pb.a, g.k, g.q, g.p, g.n, pl.ilw, pl.ilh, pl.gw - g.q + pl.ilw,
+               pl.gh - g.p + pl.ilh, 1, 1, BM};
     } else if (g.sh == 1 && g.sw == 1 && use_tma_im2col()) {
       // stride-1 dgrad is a convolution of dy with the flipped filter:
       // dx(y,x) = sum_{r',s'} dy(y + ph-(R-1) + r', x + pw-(S-1) + s') W[R-1-r'][S-1-s']
@@ -831,7 +901,7 @@ static Plan make_plan(const GemmProblem& pb) {
   // split the reduction when the tile grid cannot fill the machine
   int splits = 1;
   const int sms = num_sms();
-  if (tiles < sms && pb.stats == nullptr) {
+  if (tiles < sms && pb.stats == nullptr && !pl.remap) {
     splits = (int)cdiv(2 * sms, tiles);
     const int max_by_k = pl.num_kb / 4;
     if (splits > max_by_k) splits = max_by_k;
@@ -888,7 +958,13 @@ bool tc_eligible(const GemmProblem& pb, int dtype) {
 size_t tc_ws_bytes(const GemmProblem& pb) {
   Plan pl = make_plan(pb);
   if (!pl.ok) return 0;
-  return pl.ws_im2col + pl.ws_wpad + pl.ws_partial + 3 * 256;
+  size_t w = pl.ws_im2col + pl.ws_wpad + pl.ws_partial;
+  for (int cls = 1; cls < pl.nclass; ++cls) {
+    Plan q = make_plan(pb, cls);
+    const size_t v = q.ws_im2col + q.ws_wpad + q.ws_partial;
+    if (v > w) w = v;
+  }
+  return w + 3 * 256;
 }
 
 int32_t tc_stat_rows(const GemmProblem& pb, int dtype) {
@@ -905,11 +981,22 @@ static inline uint8_t* align256(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
 }
 
+static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st);
+
 int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (dtype != NNL_F16) return NNL_ERR_UNSUPPORTED;
-  Plan pl = make_plan(pb);
-  if (!pl.ok) return NNL_ERR_UNSUPPORTED;
+  Plan p0 = make_plan(pb, 0);
+  if (!p0.ok) return NNL_ERR_UNSUPPORTED;
   if (ws_bytes < tc_ws_bytes(pb)) return fail(NNL_ERR_INVALID_ARGUMENT, "tc workspace too small");
+  const int ncls = p0.nclass ? p0.nclass : 1;
+  for (int cls = 0; cls < ncls; ++cls) {  // strided dgrad: one GEMM per parity class
+    const int rc = run_plan(pb, cls ? make_plan(pb, cls) : p0, ws, st);
+    if (rc) return rc;
+  }
+  return NNL_OK;
+}
+
+static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   const ConvGeom& g = pb.g;
   uint8_t* w = align256(reinterpret_cast<uint8_t*>(ws));
   __half* col = nullptr;
@@ -934,7 +1021,7 @@ int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStr
     NNL_CHECK_LAUNCH();
     pl.B.ptr = wpad;
   }
-  if (pl.remap && !pb.acc) {  // pixels no output row maps to are exact zeros
+  if (pl.remap && !pb.acc && !pl.nclass) {  // 1x1 strided: unmapped pixels are exact zeros
     const int64_t n8 = (int64_t)g.n * g.h * g.w * g.c / 8;
     if ((g.c % 8) || (reinterpret_cast<uintptr_t>(pb.out) & 15))
       return fail(NNL_ERR_UNSUPPORTED, "strided dgrad output not 16 B aligned");
@@ -969,6 +1056,11 @@ int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStr
   args.out = pb.out; args.ldc = pl.ldc; args.acc = pb.acc; args.remap = pl.remap;
   args.gh = pl.gh; args.gw = pl.gw; args.ish = pl.ish; args.isw = pl.isw;
   args.ilh = pl.ilh; args.ilw = pl.ilw; args.flip = pl.flip;
+  args.rgh = pl.rgh; args.rgw = pl.rgw; args.rsh = pl.rsh; args.rsw = pl.rsw;
+  args.ra = pl.ra; args.rb = pl.rb; args.ntap = pl.ntap;
+  memcpy(args.tap_w, pl.tap_w, sizeof(args.tap_w));
+  memcpy(args.tap_offw, pl.tap_offw, sizeof(args.tap_offw));
+  memcpy(args.tap_offh, pl.tap_offh, sizeof(args.tap_offh));
   args.bias = reinterpret_cast<const __half*>(pb.bias);
   args.stats = pb.stats; args.nonfinite = pb.nonfinite;
   args.partial = pl.splits > 1 ? partial : nullptr;

@@ -21,6 +21,8 @@ CONV = [  # (B, cin, cout, k, stride, pad, hw)
     (4, 256, 512, 1, 2, 0, 14),    # 1x1 s2 dgrad: row remap + zero fill
     (16, 128, 256, 3, 1, 1, 14),   # 3x3 gather with 256-wide tiles
     (64, 64, 128, 3, 1, 1, 20),    # > 148 work units: persistent tile loop
+    (4, 64, 128, 3, 2, 1, 16),     # strided 3x3 dgrad: 4 parity-class GEMMs
+    (2, 64, 64, 3, 1, 0, 9),       # valid (pad 0) 3x3: dgrad im2col bounding box
 ]
 
 
@@ -28,7 +30,8 @@ def test_conv_backward_accumulate_mode(nnl):
     """acc=True writes q(prev + grad) (R2) on every tcgen05 path."""
     import paper_2102_06725_b200.functions as F
     _half(nnl)
-    for geom in [(2, 64, 128, 1, 2, 0, 8), (2, 64, 64, 3, 1, 1, 8), (2, 128, 256, 1, 1, 0, 6)]:
+    for geom in [(2, 64, 128, 1, 2, 0, 8), (2, 64, 64, 3, 1, 1, 8), (2, 128, 256, 1, 1, 0, 6),
+                 (2, 64, 64, 3, 2, 1, 10)]:
         b, cin, cout, k, s, p, hw = geom
         rng = np.random.default_rng(k + cout)
         x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
