@@ -159,12 +159,14 @@ int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x,
                     const float* gamma, const float* beta, const float* mean,
                     const float* var, float eps, float* save_mean, float* save_istd,
                     void* y, int fuse_relu, void* stream);
-/* relu_out (nullable): gate gy by (relu_out > 0) first (fused BN->ReLU).
+/* fused_relu: dy is the gradient of relu(BN(x)) (fused BN->ReLU); the gate
+   relu(q(gamma*xhat+beta)) > 0 is recomputed from x with the forward's exact
+   op sequence, so the ReLU output is never read.
    conv_bias_grad (nullable, dtype [c]): also reduce the ROUNDED dx over rows
    into the bias gradient of the convolution that produced x
    (functions.py:211-212), saving that convolution a pass over dx. */
 int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy,
-               const void* relu_out, const float* gamma, const float* save_mean,
+               int fused_relu, const float* gamma, const float* beta, const float* save_mean,
                const float* save_istd, int batch_stat,
                void* dx, int acc_x, float* dgamma, int acc_g, float* dbeta, int acc_b,
                void* conv_bias_grad, int acc_cb,

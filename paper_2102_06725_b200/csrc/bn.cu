@@ -18,6 +18,7 @@
 namespace nnl {
 
 constexpr int kBnThreads = 256;
+constexpr int kUnroll = 4;  // rows loaded per thread before use (memory-level parallelism)
 
 struct BnGeom {
   int vec;        // channels per thread (8 or 1)
@@ -65,12 +66,21 @@ struct VecLoad<float, 8> {
   }
 };
 
+// The fused BN->ReLU gate (z > 0) is recomputed from x with the forward's
+// exact op sequence, z = relu(q(gamma*((x-mu)*istd) + beta)), so backward
+// never reads the ReLU output (2 B/element saved in each pass).
+template <typename T>
+__device__ __forceinline__ float relu_gate(float xh, float ga, float be) {
+  return Elem<T>::ld(Elem<T>::st(__fadd_rn(__fmul_rn(ga, xh), be))) > 0.f ? 1.f : 0.f;
+}
+
 // MODE 0: (sum x, sum x^2)                               -- forward statistics
-// MODE 1: (sum gy, sum gy*xhat), gy gated by relu_out>0  -- backward reductions
+// MODE 1: (sum gy, sum gy*xhat), gy gated by the ReLU    -- backward reductions
 template <typename T, int V, int MODE>
 __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
     int64_t rows, int32_t c, int groups, int lanes, int64_t rows_per_block,
-    const T* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ relu_out,
+    const T* __restrict__ x, const T* __restrict__ dy, int relu,
+    const float* __restrict__ gamma, const float* __restrict__ beta,
     const float* __restrict__ mu, const float* __restrict__ istd, float* __restrict__ partials) {
   __shared__ float red[kBnThreads * 8 * 2];
   const int tid = threadIdx.x;
@@ -78,7 +88,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
   const int lane = tid / groups;
   const int c0 = (blockIdx.y * groups + g) * V;
   const bool active = lane < lanes && c0 < c;
-  float s1[V], s2[V], m[V], is[V];
+  float s1[V], s2[V], m[V], is[V], ga[V], be[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     s1[j] = 0.f;
@@ -86,35 +96,43 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
     if (MODE == 1 && active) {
       m[j] = mu[c0 + j];
       is[j] = istd[c0 + j];
+      ga[j] = relu ? gamma[c0 + j] : 0.f;
+      be[j] = relu ? beta[c0 + j] : 0.f;
     }
   }
   const int64_t r0 = blockIdx.x * rows_per_block;
   int64_t r1 = r0 + rows_per_block;
   if (r1 > rows) r1 = rows;
   if (active) {
-    for (int64_t r = r0 + lane; r < r1; r += lanes) {
-      float xv[V];
-      VecLoad<T, V>::load(x + r * c + c0, xv);
-      if (MODE == 0) {
+    for (int64_t rb = r0 + lane; rb < r1; rb += (int64_t)lanes * kUnroll) {
+      float xv[kUnroll][V], gv[kUnroll][V];
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          s1[j] += xv[j];
-          s2[j] = fmaf(xv[j], xv[j], s2[j]);
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t r = rb + (int64_t)u * lanes;
+        if (r < r1) {
+          VecLoad<T, V>::load(x + r * c + c0, xv[u]);
+          if (MODE == 1) VecLoad<T, V>::load(dy + r * c + c0, gv[u]);
         }
-      } else {
-        float gv[V];
-        VecLoad<T, V>::load(dy + r * c + c0, gv);
-        if (relu_out) {
-          float zv[V];
-          VecLoad<T, V>::load(relu_out + r * c + c0, zv);
+      }
 #pragma unroll
-          for (int j = 0; j < V; ++j) gv[j] = __fmul_rn(gv[j], zv[j] > 0.f ? 1.f : 0.f);
-        }
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t r = rb + (int64_t)u * lanes;
+        if (r >= r1) break;
+        if (MODE == 0) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          float xh = __fmul_rn(__fsub_rn(xv[j], m[j]), is[j]);
-          s1[j] += gv[j];
-          s2[j] += __fmul_rn(gv[j], xh);
+          for (int j = 0; j < V; ++j) {
+            s1[j] += xv[u][j];
+            s2[j] = fmaf(xv[u][j], xv[u][j], s2[j]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const float xh = __fmul_rn(__fsub_rn(xv[u][j], m[j]), is[j]);
+            const float gy = relu ? __fmul_rn(gv[u][j], relu_gate<T>(xh, ga[j], be[j]))
+                                  : gv[u][j];
+            s1[j] += gy;
+            s2[j] += __fmul_rn(gy, xh);
+          }
         }
       }
     }
@@ -252,7 +270,6 @@ struct VecStore<float, 8> {
 // reductions: each thread owns V channels for the whole launch, so the
 // per-channel constants live in registers and the inner loop has no index
 // division (the first version's int64 `i % C` per element cost 5x).
-constexpr int kUnroll = 4;
 
 // y = q(gamma * ((x - mu) * istd) + beta), then ReLU on the stored value
 template <typename T, int V>
@@ -308,8 +325,8 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd_apply(
 template <typename T, int V>
 __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
     int64_t rows, int32_t c, int groups, int lanes, int64_t rows_per_block,
-    const T* __restrict__ x, const T* __restrict__ dy, const T* __restrict__ relu_out,
-    const float* __restrict__ gamma, const float* __restrict__ mu,
+    const T* __restrict__ x, const T* __restrict__ dy, int relu,
+    const float* __restrict__ gamma, const float* __restrict__ beta, const float* __restrict__ mu,
     const float* __restrict__ istd, const float* __restrict__ gsum, int batch_stat,
     T* __restrict__ dx, int acc, float* __restrict__ bias_part) {
   __shared__ float red[kBnThreads * 8];
@@ -317,14 +334,16 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
   const int c0 = (blockIdx.y * groups + g) * V;
   const bool active = lane < lanes && c0 < c;
   const float fn = (float)rows;
-  float m[V], is[V], gg[V], gn[V], gb[V], gy2[V], cs[V];
+  float m[V], is[V], gg[V], gn[V], gb[V], gy2[V], cs[V], ga[V], be[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     cs[j] = 0.f;
     if (active) {
       m[j] = mu[c0 + j];
       is[j] = istd[c0 + j];
-      gg[j] = __fmul_rn(gamma[c0 + j], is[j]);   // g = gamma * istd
+      ga[j] = gamma[c0 + j];
+      be[j] = relu ? beta[c0 + j] : 0.f;
+      gg[j] = __fmul_rn(ga[j], is[j]);           // g = gamma * istd
       gn[j] = __fdiv_rn(gg[j], fn);              // g / n
       gb[j] = gsum[c0 + j];                      // gbeta
       gy2[j] = gsum[c + c0 + j];                 // ggamma
@@ -340,14 +359,17 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
         const int64_t r = rb + (int64_t)u * lanes;
         if (r < r1) {
           VecLoad<T, V>::load(dy + r * c + c0, gv[u]);
-          if (batch_stat) VecLoad<T, V>::load(x + r * c + c0, xv[u]);
-          if (relu_out) {
-            float zv[V];
-            VecLoad<T, V>::load(relu_out + r * c + c0, zv);
-#pragma unroll
-            for (int j = 0; j < V; ++j) gv[u][j] = __fmul_rn(gv[u][j], zv[j] > 0.f ? 1.f : 0.f);
-          }
+          if (batch_stat || relu) VecLoad<T, V>::load(x + r * c + c0, xv[u]);
         }
+      }
+      if (relu) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const float xh = __fmul_rn(__fsub_rn(xv[u][j], m[j]), is[j]);
+            gv[u][j] = __fmul_rn(gv[u][j], relu_gate<T>(xh, ga[j], be[j]));
+          }
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -433,16 +455,16 @@ static size_t bn_ws_bytes(int64_t rows, int32_t c) {
 
 template <typename T, int MODE>
 static int launch_partials(int64_t rows, int32_t c, const BnGeom& g, int64_t bx, const T* x,
-                           const T* dy, const T* relu, const float* mu, const float* istd,
-                           float* partials, cudaStream_t st) {
+                           const T* dy, int relu, const float* gamma, const float* beta,
+                           const float* mu, const float* istd, float* partials, cudaStream_t st) {
   int64_t rpb = (rows + bx - 1) / bx;
   dim3 grid((unsigned)bx, (unsigned)g.slabs);
   if (g.vec == 8)
     k_bn_partials<T, 8, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, mu, istd, partials);
+                                                           relu, gamma, beta, mu, istd, partials);
   else
     k_bn_partials<T, 1, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, mu, istd, partials);
+                                                           relu, gamma, beta, mu, istd, partials);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
@@ -497,8 +519,8 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
     float* p = (float*)ws;
     int rc;
     NNL_DISPATCH_DTYPE(dtype, T, {
-      rc = launch_partials<T, 0>(rows, c, g, bx, (const T*)x, nullptr, nullptr, nullptr, nullptr,
-                                 p, st);
+      rc = launch_partials<T, 0>(rows, c, g, bx, (const T*)x, nullptr, 0, nullptr, nullptr,
+                                 nullptr, nullptr, p, st);
     });
     if (rc) return rc;
     parts = p;
@@ -532,22 +554,23 @@ int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x, const flo
 }
 
 int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy,
-               const void* relu_out, const float* gamma, const float* save_mean,
+               int fused_relu, const float* gamma, const float* beta, const float* save_mean,
                const float* save_istd, int batch_stat, void* dx, int acc_x, float* dgamma,
                int acc_g, float* dbeta, int acc_b, void* conv_bias_grad, int acc_cb,
                int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (ws_bytes < bn_ws_bytes(rows, c))
     return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
-  BnGeom g = bn_geom(c, al16(x) && al16(dy) && al16(relu_out) && al16(dx));
+  if (fused_relu && !beta) return fail(NNL_ERR_INVALID_ARGUMENT, "fused ReLU needs beta");
+  BnGeom g = bn_geom(c, al16(x) && al16(dy) && al16(dx));
   int64_t bx = bn_blocks_x(rows, g);
   float* parts = (float*)ws;
   float* gsum = parts + bx * 2 * c;
   float* bparts = gsum + 2 * c;
   int rc;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, (const T*)relu_out,
-                               save_mean, save_istd, parts, st);
+    rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, fused_relu, gamma,
+                               beta, save_mean, save_istd, parts, st);
   });
   if (rc) return rc;
   k_bn_finalize_bwd<<<(c + 31) / 32, 1024, 0, st>>>(parts, (int32_t)bx, c, gsum, dgamma, acc_g,
@@ -560,11 +583,11 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
   NNL_DISPATCH_DTYPE(dtype, T, {
     if (g.vec == 8)
       k_bn_bwd_apply<T, 8><<<grid, kBnThreads, 0, st>>>(
-          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, (const T*)relu_out, gamma,
+          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
           save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
     else
       k_bn_bwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(
-          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, (const T*)relu_out, gamma,
+          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
           save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
     NNL_CHECK_LAUNCH();
     if (bp) {

@@ -46,7 +46,9 @@ struct Cfg {
   static constexpr int PIPE = STAGES * (A_BYTES + B_BYTES);
   static constexpr int RED_BYTES = 4 * BN * 2 * 4;
   static constexpr int BIAS_BYTES = BN * 4;
-  static constexpr int SMEM = PIPE + 1024 + RED_BYTES + BIAS_BYTES + 1024;
+  static constexpr int MAX_STAT_N = 2048;  // per-CTA BN statistics accumulator [2][N]
+  static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
+  static constexpr int SMEM = PIPE + 1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + 1024;
 };
 
 struct TcArgs {
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* red = reinterpret_cast<float*>(smem + C::PIPE + 1024);
   float* bias_s = reinterpret_cast<float*>(smem + C::PIPE + 1024 + C::RED_BYTES);
+  float* stat_s = reinterpret_cast<float*>(smem + C::PIPE + 1024 + C::RED_BYTES + C::BIAS_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ConvGeom& g = a.g;
@@ -379,6 +382,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue
     const int wq = warp & 3;
     const int tid = threadIdx.x - 256;
+    if (a.stats) {
+      for (int j = tid; j < 2 * C::MAX_STAT_N; j += 128) stat_s[j] = 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
     int t = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++t) {
       const Unit w = decode_unit(a, u);
@@ -502,10 +509,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             t1 += red[(q * BN + col) * 2 + 0];
             t2 += red[(q * BN + col) * 2 + 1];
           }
-          a.stats[((int64_t)w.tm * 2 + 0) * a.N + n0 + col] = t1;
-          a.stats[((int64_t)w.tm * 2 + 1) * a.N + n0 + col] = t2;
+          // per-CTA running sums, in this CTA's fixed tile order (deterministic)
+          stat_s[n0 + col] += t1;
+          stat_s[C::MAX_STAT_N + n0 + col] += t2;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+    if (a.stats) {  // one partial row per CTA: stats[blockIdx.x][2][N]
+      for (int col = tid; col < a.N; col += 128) {
+        a.stats[((int64_t)blockIdx.x * 2 + 0) * a.N + col] = stat_s[col];
+        a.stats[((int64_t)blockIdx.x * 2 + 1) * a.N + col] = stat_s[C::MAX_STAT_N + col];
       }
     }
   }
@@ -973,8 +987,9 @@ int32_t tc_stat_rows(const GemmProblem& pb, int dtype) {
   float dummy;
   q.stats = &dummy;  // stats disable split-K
   Plan pl = make_plan(q);
-  if (!pl.ok || pb.mode != kFprop || pb.g.affine) return 0;
-  return (int32_t)cdiv(pl.M, BM);
+  if (!pl.ok || pb.mode != kFprop || pb.g.affine || pl.N > Cfg<64>::MAX_STAT_N) return 0;
+  // one partial row per persistent CTA
+  return pl.units < num_sms() ? pl.units : num_sms();
 }
 
 static inline uint8_t* align256(uint8_t* p) {

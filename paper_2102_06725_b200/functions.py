@@ -424,12 +424,13 @@ class BatchNormalization(FunctionImpl):
         self._forward(node, ys[0], relu=False)
 
     def forward_fused(self, node, relu_node, stats):
-        relu_node.state["keep_output"] = True
+        # backward recomputes the ReLU gate from x, so the output may be released
         self._forward(node, relu_node.outputs[0].data, relu=True)
 
-    def _backward(self, node, gy: NdArray, relu_out, gxs, acc):
+    def _backward(self, node, gy: NdArray, fused_relu: bool, gxs, acc):
         x = node.inputs[0].data
         gamma = node.inputs[1].data
+        beta = node.inputs[2].data
         c = x.shape[1]
         rows = self._rows(x)
         ws = _lib.workspace(_lib.lib().nnl_bn_workspace_size(rows, c))
@@ -437,7 +438,8 @@ class BatchNormalization(FunctionImpl):
         cbias = None
         if gxs[0] is not None and conv is not None and conv.state.get("bias_by_bn"):
             cbias = conv.inputs[2].grad.ptr  # sole consumer: first contribution overwrites
-        _lib.call("nnl_bn_bwd", x.code, rows, c, x.ptr, gy.ptr, relu_out, gamma.ptr,
+        _lib.call("nnl_bn_bwd", x.code, rows, c, x.ptr, gy.ptr, 1 if fused_relu else 0,
+                  gamma.ptr, beta.ptr,
                   node.state["mean"].data_ptr(), node.state["istd"].data_ptr(),
                   1 if self.batch_stat else 0,
                   gxs[0].ptr if gxs[0] is not None else None, _flag(acc[0]),
@@ -446,11 +448,10 @@ class BatchNormalization(FunctionImpl):
                   cbias, 0, node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
 
     def backward(self, node, gys, gxs, acc):
-        self._backward(node, gys[0], None, gxs, acc)
+        self._backward(node, gys[0], False, gxs, acc)
 
     def backward_fused(self, node, relu_node, gxs, acc):
-        z = relu_node.outputs[0]
-        self._backward(node, z.grad, z.data.ptr, gxs, acc)
+        self._backward(node, relu_node.outputs[0].grad, True, gxs, acc)
 
     def backward_reads_input(self, index):
         return index in (0, 1)

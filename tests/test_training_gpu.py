@@ -210,14 +210,20 @@ def test_resnet18_cifar_step_vs_oracle(nnl, half):
     assert abs(got - want) <= (2e-2 if half else 1e-4) * max(1, abs(want))
     params = tr.models[0].trainable()
     assert set(params) == set(grads)
+    # Deep-chain tolerance, relative to each tensor's max: BN backward at 64
+    # elements/channel (4x4 maps, batch 4) amplifies summation-order differences
+    # (n*gy - sum(gy) - xhat*sum(gy*xhat)) layer after layer, and under Half every
+    # activation/gradient is re-rounded to fp16.  Conv biases feeding a train-mode
+    # BN have a mathematically zero gradient (pure rounding noise on both sides),
+    # hence the absolute floor relative to the largest gradient of the network.
+    gscale = max(np.abs(v.grad).max() for v in params.values())
+    floor = (1e-2 if half else 1e-3) * gscale
+    tol = 0.15 if half else 1e-2
     for k, v in params.items():
-        scale = np.abs(v.grad).max() + 1e-6
-        # gradients through 20 BN layers: compare relative to each tensor's scale
-        err = np.abs(grads[k] - v.grad).max() / scale
-        # Deep-chain tolerance, relative to each tensor's max: BN backward at 64
-        # elements/channel (4x4 maps, batch 4) amplifies summation-order
-        # differences (n*gy - sum(gy) - xhat*sum(gy*xhat)) layer after layer,
-        # and under Half every activation/gradient is re-rounded to fp16.
-        assert err < (0.15 if half else 1e-2), (k, err)
-        werr = np.abs(weights[k] - v.value).max() / (np.abs(v.value).max() + 1e-6)
-        assert werr < (2e-2 if half else 1e-2), (k, werr)
+        denom = max(np.abs(v.grad).max(), floor)
+        err = np.abs(grads[k] - v.grad).max() / denom
+        assert err < tol, (k, err)
+        # w1 - w0 = -lr * g: the weight difference follows the gradient difference
+        ulp = 2.0 ** -10 * np.abs(v.value).max() if half else 0.0  # fp16 weight rounding
+        werr = np.abs(weights[k] - v.value).max() / (0.1 * denom + ulp)
+        assert werr < 1.5 * tol, (k, werr)
