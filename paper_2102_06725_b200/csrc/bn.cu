@@ -27,9 +27,12 @@ struct BnGeom {
   int slabs;      // grid.y
 };
 
-static BnGeom bn_geom(int32_t c, bool vec_ok) {
+// vmax 8 for the forward kernels; 4 for the backward ones, whose per-channel
+// state (9 constants + 2 loaded rows x unroll) would otherwise need ~180
+// registers and drop the SM to one 256-thread block.
+static BnGeom bn_geom(int32_t c, bool vec_ok, int vmax = 8) {
   BnGeom g;
-  g.vec = (vec_ok && c % 8 == 0) ? 8 : 1;
+  g.vec = (vec_ok && c % vmax == 0) ? vmax : 1;
   int total_groups = c / g.vec;
   g.groups = total_groups < kBnThreads ? total_groups : kBnThreads;
   g.lanes = kBnThreads / g.groups;
@@ -54,6 +57,22 @@ struct VecLoad<__half, 8> {
       out[2 * j] = f.x;
       out[2 * j + 1] = f.y;
     }
+  }
+};
+template <>
+struct VecLoad<__half, 4> {
+  static __device__ __forceinline__ void load(const __half* p, float* out) {
+    uint2 u = *reinterpret_cast<const uint2*>(p);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+    float2 a = __half22float2(h[0]), b = __half22float2(h[1]);
+    out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
+  }
+};
+template <>
+struct VecLoad<float, 4> {
+  static __device__ __forceinline__ void load(const float* p, float* out) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
   }
 };
 template <>
@@ -259,6 +278,18 @@ struct VecStore<__half, 8> {
   }
 };
 template <>
+struct VecStore<__half, 4> {
+  static __device__ __forceinline__ void store(__half* p, const __half* v) {
+    *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(v);
+  }
+};
+template <>
+struct VecStore<float, 4> {
+  static __device__ __forceinline__ void store(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <>
 struct VecStore<float, 8> {
   static __device__ __forceinline__ void store(float* p, const float* v) {
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -302,7 +333,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd_apply(
     for (int u = 0; u < kUnroll; ++u) {
       const int64_t r = rb + (int64_t)u * lanes;
       if (r >= r1) break;
-      T out[V];
+      __align__(16) T out[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const float xh = __fmul_rn(__fsub_rn(xv[u][j], m[j]), is[j]);
@@ -377,7 +408,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
         if (r >= r1) break;
         float pv[V];
         if (acc) VecLoad<T, V>::load(dx + r * c + c0, pv);
-        T out[V];
+        __align__(16) T out[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) {
           float res;
@@ -445,11 +476,11 @@ struct BnWs {
 };
 
 static size_t bn_ws_bytes(int64_t rows, int32_t c) {
-  BnGeom g = bn_geom(c, true);
-  int64_t bx = bn_blocks_x(rows, g);
-  BnGeom g1 = bn_geom(c, false);
-  int64_t bx1 = bn_blocks_x(rows, g1);
-  if (bx1 > bx) bx = bx1;
+  int64_t bx = 1;
+  for (int v : {8, 4, 1}) {
+    const int64_t b = bn_blocks_x(rows, bn_geom(c, v > 1, v));
+    if (b > bx) bx = b;
+  }
   return (size_t)(2 * bx * 2 * c + 2 * c) * sizeof(float) + 256;
 }
 
@@ -461,6 +492,9 @@ static int launch_partials(int64_t rows, int32_t c, const BnGeom& g, int64_t bx,
   dim3 grid((unsigned)bx, (unsigned)g.slabs);
   if (g.vec == 8)
     k_bn_partials<T, 8, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
+                                                           relu, gamma, beta, mu, istd, partials);
+  else if (g.vec == 4)
+    k_bn_partials<T, 4, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
                                                            relu, gamma, beta, mu, istd, partials);
   else
     k_bn_partials<T, 1, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
@@ -562,7 +596,7 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
   if (ws_bytes < bn_ws_bytes(rows, c))
     return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
   if (fused_relu && !beta) return fail(NNL_ERR_INVALID_ARGUMENT, "fused ReLU needs beta");
-  BnGeom g = bn_geom(c, al16(x) && al16(dy) && al16(dx));
+  BnGeom g = bn_geom(c, al16(x) && al16(dy) && al16(dx), 4);
   int64_t bx = bn_blocks_x(rows, g);
   float* parts = (float*)ws;
   float* gsum = parts + bx * 2 * c;
@@ -581,8 +615,8 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
   dim3 grid((unsigned)bx, (unsigned)g.slabs);
   float* bp = conv_bias_grad ? bparts : nullptr;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    if (g.vec == 8)
-      k_bn_bwd_apply<T, 8><<<grid, kBnThreads, 0, st>>>(
+    if (g.vec == 4)
+      k_bn_bwd_apply<T, 4><<<grid, kBnThreads, 0, st>>>(
           rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
           save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
     else
