@@ -13,6 +13,7 @@
 // Op order in every f32 expression follows the reference line by line with
 // explicit _rn intrinsics (no FMA contraction), so results differ from numpy
 // only through the summation order of the statistics.
+#include "bn_stream.cuh"
 #include "common.cuh"
 
 namespace nnl {
@@ -180,15 +181,20 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
   }
 }
 
-// Fixed-order f64 reduction of partial rows [R][2][C]: block = 32 channel
-// columns x 32 row lanes.
+// Fixed-order f64 reduction of partial rows [R][2][C]: block = 8 channel
+// columns x 128 row lanes (1024 threads), so even C = 64 gets 8 blocks and
+// each lane sums only R/128 rows.  Column index: blockIdx.x*8 + (tid & 7).
+constexpr int kRedCols = 8, kRedLanes = 128;
+__device__ __forceinline__ int red_channel() { return blockIdx.x * kRedCols + (threadIdx.x & 7); }
+__device__ __forceinline__ bool red_leader() { return (threadIdx.x >> 3) == 0; }
+
 __device__ __forceinline__ void reduce_partials(const float* __restrict__ partials, int32_t R,
                                                 int32_t c, int ch, double& a, double& b) {
-  __shared__ double sa[32][33], sb[32][33];
-  const int col = threadIdx.x & 31, lane = threadIdx.x >> 5;
+  __shared__ double sa[kRedLanes][kRedCols + 1], sb[kRedLanes][kRedCols + 1];
+  const int col = threadIdx.x & 7, lane = threadIdx.x >> 3;
   double x = 0.0, y = 0.0;
   if (ch < c) {
-    for (int r = lane; r < R; r += 32) {
+    for (int r = lane; r < R; r += kRedLanes) {
       x += (double)partials[(int64_t)r * 2 * c + ch];
       y += (double)partials[(int64_t)r * 2 * c + c + ch];
     }
@@ -199,7 +205,7 @@ __device__ __forceinline__ void reduce_partials(const float* __restrict__ partia
   a = 0.0;
   b = 0.0;
   if (lane == 0) {
-    for (int l = 0; l < 32; ++l) {
+    for (int l = 0; l < kRedLanes; ++l) {
       a += sa[l][col];
       b += sb[l][col];
     }
@@ -211,10 +217,10 @@ __global__ void __launch_bounds__(1024) k_bn_finalize_fwd(
     const float* __restrict__ partials, int32_t R, int32_t c, int64_t count,
     float* __restrict__ running_mean, float* __restrict__ running_var, float eps, float momentum,
     float* __restrict__ save_mean, float* __restrict__ save_istd) {
-  const int ch = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ch = red_channel();
   double s1, s2;
   reduce_partials(partials, R, c, ch, s1, s2);
-  if ((threadIdx.x >> 5) == 0 && ch < c) {
+  if (red_leader() && ch < c) {
     double mean = s1 / (double)count;
     double var = s2 / (double)count - mean * mean;
     if (var < 0.0) var = 0.0;
@@ -243,10 +249,10 @@ __global__ void __launch_bounds__(1024) k_bn_finalize_bwd(
     const float* __restrict__ partials, int32_t R, int32_t c, float* __restrict__ gsum,
     float* __restrict__ dgamma, int acc_g, float* __restrict__ dbeta, int acc_b,
     int32_t* __restrict__ nonfinite) {
-  const int ch = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ch = red_channel();
   double s1, s2;
   reduce_partials(partials, R, c, ch, s1, s2);
-  if ((threadIdx.x >> 5) == 0 && ch < c) {
+  if (red_leader() && ch < c) {
     float gbeta = (float)s1, ggamma = (float)s2;
     gsum[ch] = gbeta;
     gsum[c + ch] = ggamma;
@@ -450,10 +456,10 @@ template <typename T>
 __global__ void __launch_bounds__(1024) k_bn_bias_finalize(const float* __restrict__ partials,
                                                            int32_t R, int32_t c, T* __restrict__ db,
                                                            int acc, int32_t* __restrict__ nonfinite) {
-  const int ch = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int ch = red_channel();
   double s1, s2;
   reduce_partials(partials, R, c, ch, s1, s2);
-  if ((threadIdx.x >> 5) == 0 && ch < c) {
+  if (red_leader() && ch < c) {
     write_out(db + ch, (float)s1, acc != 0);
     if (nonfinite && !isfinite(Elem<T>::load(db + ch))) atomicOr(nonfinite, 1);
   }
@@ -481,6 +487,11 @@ static size_t bn_ws_bytes(int64_t rows, int32_t c) {
     const int64_t b = bn_blocks_x(rows, bn_geom(c, v > 1, v));
     if (b > bx) bx = b;
   }
+  if (c % 8 == 0 && c <= 2048)
+    for (int m : {BNS_STATS_F, BNS_STATS_B, BNS_APPLY_B}) {
+      const int64_t b = bn_stream_rows(m, rows, c);
+      if (b > bx) bx = b;
+    }
   return (size_t)(2 * bx * 2 * c + 2 * c) * sizeof(float) + 256;
 }
 
@@ -532,6 +543,11 @@ static int launch_fwd_apply(int64_t rows, int32_t c, const BnGeom& g, const T* x
   return NNL_OK;
 }
 
+static bool use_stream(int dtype, int64_t rows, int32_t c, const void* a, const void* b,
+                       const void* d) {
+  return dtype == NNL_F16 && bn_stream_ok(rows, c, a, b, d);
+}
+
 extern "C" {
 
 int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const float* gamma,
@@ -543,27 +559,40 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
     return fail(NNL_ERR_DEGENERATE_BATCH, "cannot take batch statistics over %lld element(s)",
                 (long long)rows);
   cudaStream_t st = as_stream(stream);
+  const bool stream_ok = use_stream(dtype, rows, c, x, y, nullptr);
   BnGeom g = bn_geom(c, al16(x) && al16(y));
   const float* parts = stat_partials;
   int32_t R = n_partials;
+  int rc = NNL_OK;
   if (!parts) {
     if (ws_bytes < bn_ws_bytes(rows, c))
       return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
-    int64_t bx = bn_blocks_x(rows, g);
     float* p = (float*)ws;
-    int rc;
-    NNL_DISPATCH_DTYPE(dtype, T, {
-      rc = launch_partials<T, 0>(rows, c, g, bx, (const T*)x, nullptr, 0, nullptr, nullptr,
-                                 nullptr, nullptr, p, st);
-    });
+    if (stream_ok) {
+      BnStreamArgs a = {};
+      a.rows = rows; a.c = c; a.x = (const __half*)x; a.partials = p;
+      rc = bn_stream_launch(BNS_STATS_F, a, st);
+      R = bn_stream_rows(BNS_STATS_F, rows, c);
+    } else {
+      const int64_t bx = bn_blocks_x(rows, g);
+      NNL_DISPATCH_DTYPE(dtype, T, {
+        rc = launch_partials<T, 0>(rows, c, g, bx, (const T*)x, nullptr, 0, nullptr, nullptr,
+                                   nullptr, nullptr, p, st);
+      });
+      R = (int32_t)bx;
+    }
     if (rc) return rc;
     parts = p;
-    R = (int32_t)bx;
   }
-  k_bn_finalize_fwd<<<(c + 31) / 32, 1024, 0, st>>>(parts, R, c, rows, running_mean, running_var,
-                                                   eps, momentum, save_mean, save_istd);
+  k_bn_finalize_fwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+      parts, R, c, rows, running_mean, running_var, eps, momentum, save_mean, save_istd);
   NNL_CHECK_LAUNCH();
-  int rc;
+  if (stream_ok) {
+    BnStreamArgs a = {};
+    a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)y; a.gamma = gamma;
+    a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fuse_relu;
+    return bn_stream_launch(BNS_APPLY_F, a, st);
+  }
   NNL_DISPATCH_DTYPE(dtype, T, {
     rc = launch_fwd_apply<T>(rows, c, g, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y,
                              fuse_relu, st);
@@ -578,6 +607,12 @@ int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x, const flo
   k_bn_eval_stats<<<(c + 255) / 256, 256, 0, st>>>(c, mean, var, eps, save_mean, save_istd);
   NNL_CHECK_LAUNCH();
   if (rows * c <= 0) return NNL_OK;
+  if (use_stream(dtype, rows, c, x, y, nullptr)) {
+    BnStreamArgs a = {};
+    a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)y; a.gamma = gamma;
+    a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fuse_relu;
+    return bn_stream_launch(BNS_APPLY_F, a, st);
+  }
   BnGeom g = bn_geom(c, al16(x) && al16(y));
   int rc;
   NNL_DISPATCH_DTYPE(dtype, T, {
@@ -596,40 +631,61 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
   if (ws_bytes < bn_ws_bytes(rows, c))
     return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
   if (fused_relu && !beta) return fail(NNL_ERR_INVALID_ARGUMENT, "fused ReLU needs beta");
+  const bool stream_ok = use_stream(dtype, rows, c, x, dy, dx);
   BnGeom g = bn_geom(c, al16(x) && al16(dy) && al16(dx), 4);
-  int64_t bx = bn_blocks_x(rows, g);
+  const int64_t bx = stream_ok ? bn_stream_rows(BNS_STATS_B, rows, c) : bn_blocks_x(rows, g);
   float* parts = (float*)ws;
   float* gsum = parts + bx * 2 * c;
   float* bparts = gsum + 2 * c;
-  int rc;
-  NNL_DISPATCH_DTYPE(dtype, T, {
-    rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, fused_relu, gamma,
-                               beta, save_mean, save_istd, parts, st);
-  });
+  int rc = NNL_OK;
+  if (stream_ok) {
+    BnStreamArgs a = {};
+    a.rows = rows; a.c = c; a.x = (const __half*)x; a.dy = (const __half*)dy; a.gamma = gamma;
+    a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fused_relu; a.partials = parts;
+    rc = bn_stream_launch(BNS_STATS_B, a, st);
+  } else {
+    NNL_DISPATCH_DTYPE(dtype, T, {
+      rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, fused_relu, gamma,
+                                 beta, save_mean, save_istd, parts, st);
+    });
+  }
   if (rc) return rc;
-  k_bn_finalize_bwd<<<(c + 31) / 32, 1024, 0, st>>>(parts, (int32_t)bx, c, gsum, dgamma, acc_g,
-                                                   dbeta, acc_b, nonfinite);
+  k_bn_finalize_bwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+      parts, (int32_t)bx, c, gsum, dgamma, acc_g, dbeta, acc_b, nonfinite);
   NNL_CHECK_LAUNCH();
   if (!dx) return NNL_OK;
-  const int64_t rpb = (rows + bx - 1) / bx;
-  dim3 grid((unsigned)bx, (unsigned)g.slabs);
   float* bp = conv_bias_grad ? bparts : nullptr;
-  NNL_DISPATCH_DTYPE(dtype, T, {
-    if (g.vec == 4)
-      k_bn_bwd_apply<T, 4><<<grid, kBnThreads, 0, st>>>(
-          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
-          save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
-    else
-      k_bn_bwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(
-          rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
-          save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
+  int32_t brows = (int32_t)bx;
+  if (stream_ok) {
+    BnStreamArgs a = {};
+    a.rows = rows; a.c = c; a.x = (const __half*)x; a.dy = (const __half*)dy; a.out = (__half*)dx;
+    a.gamma = gamma; a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.gsum = gsum;
+    a.partials = bp; a.relu = fused_relu; a.acc = acc_x; a.batch_stat = batch_stat;
+    rc = bn_stream_launch(BNS_APPLY_B, a, st);
+    if (rc) return rc;
+    brows = bn_stream_rows(BNS_APPLY_B, rows, c);
+  } else {
+    const int64_t rpb = (rows + bx - 1) / bx;
+    dim3 grid((unsigned)bx, (unsigned)g.slabs);
+    NNL_DISPATCH_DTYPE(dtype, T, {
+      if (g.vec == 4)
+        k_bn_bwd_apply<T, 4><<<grid, kBnThreads, 0, st>>>(
+            rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
+            save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
+      else
+        k_bn_bwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(
+            rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
+            save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
+    });
     NNL_CHECK_LAUNCH();
-    if (bp) {
-      k_bn_bias_finalize<T><<<(c + 31) / 32, 1024, 0, st>>>(bp, (int32_t)bx, c,
-                                                            (T*)conv_bias_grad, acc_cb, nonfinite);
-      NNL_CHECK_LAUNCH();
-    }
-  });
+  }
+  if (bp) {
+    NNL_DISPATCH_DTYPE(dtype, T, {
+      k_bn_bias_finalize<T><<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+          bp, brows, c, (T*)conv_bias_grad, acc_cb, nonfinite);
+    });
+    NNL_CHECK_LAUNCH();
+  }
   return NNL_OK;
 }
 

@@ -1,0 +1,34 @@
+// Streaming BatchNormalization kernels (bn_stream.cu), used by bn.cu for fp16
+// activations with C % 8 == 0 and C <= 2048.
+#pragma once
+#include "common.cuh"
+
+namespace nnl {
+
+enum BnStreamMode { BNS_STATS_F = 0, BNS_APPLY_F = 1, BNS_STATS_B = 2, BNS_APPLY_B = 3 };
+
+struct BnStreamArgs {
+  int64_t rows;
+  int32_t c;
+  int32_t chunk_rows;  // filled by bn_stream_launch
+  int64_t nchunks;     // filled by bn_stream_launch
+  const __half* x;
+  const __half* dy;
+  __half* out;
+  const float* gamma;
+  const float* beta;
+  const float* mu;
+  const float* istd;
+  const float* gsum;   // [2][C] gbeta, ggamma (APPLY_B)
+  float* partials;     // [grid][2][C] (STATS_*, APPLY_B bias sums)
+  int relu;
+  int acc;
+  int batch_stat;
+};
+
+bool bn_stream_ok(int64_t rows, int32_t c, const void* a, const void* b, const void* d);
+// number of partial rows the launch writes (its grid size)
+int bn_stream_rows(int mode, int64_t rows, int32_t c);
+int bn_stream_launch(int mode, const BnStreamArgs& a, cudaStream_t st);
+
+}  // namespace nnl

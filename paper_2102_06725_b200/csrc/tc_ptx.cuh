@@ -70,6 +70,16 @@ __device__ __forceinline__ void tma_load_im2col(void* dst, const void* tmap, uin
       : "memory");
 }
 
+// contiguous bulk copy global -> shared (bytes % 16 == 0, 16 B aligned)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---- cp.async gathers (16 B, zero-filled when src_bytes == 0) -------------------
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),

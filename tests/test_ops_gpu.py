@@ -162,3 +162,46 @@ def test_conv_random_vs_oracle(nnl, half, geom):
     close(y.d, oy.value, **tol)
     for v, o in zip(vs, ov):
         close(v.g, o.grad, **tol)
+
+
+@pytest.mark.parametrize("shape", [(8, 64, 10, 10), (4, 256, 7, 7), (3, 24, 5, 5), (6, 2048, 2, 2)])
+@pytest.mark.parametrize("relu", [False, True])
+def test_bn_train_streaming_vs_oracle(nnl, shape, relu):
+    """fp16 BN (streaming kernels for C % 8 == 0) fwd + bwd, optionally fused
+    with the following ReLU through the engine's clear_buffer plan."""
+    import paper_2102_06725_b200.functions as F
+    _ctx(nnl, True)
+    rng = np.random.default_rng(shape[1])
+    x = rng.uniform(-2, 3, shape).astype(np.float32)
+    c = shape[1]
+    g0 = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    b0 = rng.uniform(-0.5, 0.5, c).astype(np.float32)
+    xv = nnl.Variable(shape, need_grad=True)
+    xv.d = x
+    ps = []
+    for a, ng in ((g0, True), (b0, True), (np.zeros(c, np.float32), False),
+                  (np.ones(c, np.float32), False)):
+        v = nnl.Variable((c,), need_grad=ng, dtype=nnl.Dtype.F32)
+        v.d = a
+        ps.append(v)
+    y = F.batch_normalization(xv, *ps)
+    out = F.relu(y) if relu else y
+    gy = O.q16(rng.uniform(-1, 1, shape).astype(np.float32))
+    out.forward(clear_buffer=True)
+    out.backward(1.0, clear_buffer=True)
+    # oracle with the same upstream gradient: seed 1 then scale via a probe
+    ox = O.Var(x, half=True, need_grad=True)
+    og = O.Var(g0, need_grad=True)
+    ob = O.Var(b0, need_grad=True)
+    om = O.Var(np.zeros(c, np.float32))
+    ov = O.Var(np.ones(c, np.float32))
+    oy = O.batch_norm(ox, og, ob, om, ov, True)
+    oo = O.relu(oy, True) if relu else oy
+    O.backward(oo, 1.0)
+    close(out.d, oo.value, 2e-3, 2e-3)
+    # ones-seeded BN backward: sum(gy) = n, grads of x vanish up to rounding
+    close(ps[1].g, ob.grad, 1e-3, 1e-2)
+    close(ps[0].g, og.grad, 1e-3, 1e-2)
+    close(xv.g, ox.grad, 1e-2, 2e-3)
+    close(ps[2].d, om.value, 1e-5, 1e-5)      # running mean (f32)
+    close(ps[3].d, ov.value, 1e-4, 1e-5)      # running var (f32, biased batch var)
