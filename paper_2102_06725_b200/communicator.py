@@ -411,9 +411,39 @@ class DataParallelTrainer:
             rep.solver.update()
         return loss
 
+    def capture_graph(self) -> None:
+        """Record one resident step into a CUDA graph; later `step_resident`
+        calls replay it (removes the per-node launch overhead).
+
+        Call after at least one warm-up step (all buffers, workspaces and
+        tensor maps are then allocated at fixed addresses).  Single process
+        only; the host-synchronous paths (clip_norm, host scaler) are refused."""
+        if self.distributed or self.n_workers != 1:
+            raise NotImplementedError("graph capture is implemented for one replica per process")
+        rep = self.replicas[0]
+        if rep.dscaler is None and self.static_scale is None and rep.scaler is not None:
+            raise NotImplementedError("host-synchronous loss scaling cannot be captured")
+        t = _lib.torch()
+        side = t.cuda.Stream()
+        side.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(side):
+            self._work(rep, 0, None, None, lambda r: None)  # warm on the capture stream
+        t.cuda.current_stream().wait_stream(side)
+        g = t.cuda.CUDAGraph()
+        before = _lib.lib().nnl_launch_count(0)
+        with t.cuda.graph(g, stream=side):
+            self._work(rep, 0, None, None, lambda r: None)
+        t.cuda.current_stream().wait_stream(side)
+        self.graph_kernels = int(_lib.lib().nnl_launch_count(0) - before)  # libnnl kernels/step
+        self._graph = g
+
     def step_resident(self) -> None:
         """One step on the inputs already resident on the device: no host
         transfer and no loss read-back (the benchmark's device-side `value`)."""
+        graph = getattr(self, "_graph", None)
+        if graph is not None:
+            graph.replay()
+            return
         if self.distributed:
             rep = self.replicas[0]
 
@@ -454,6 +484,13 @@ class DataParallelTrainer:
             self.comm._dist.all_reduce(lv)
             return float(lv.item()) / self.n_workers
         if not self.distributed and self.n_workers == 1:
+            graph = getattr(self, "_graph", None)
+            if graph is not None:  # inputs through .d (H2D), then the recorded step
+                rep = self.replicas[0]
+                rep.handles["x"].d = x_batch[:self.shard_size]
+                rep.handles["label"].d = label_batch[:self.shard_size]
+                graph.replay()
+                return float(rep.handles["loss"].d)
             loss = self._work(self.replicas[0], 0, x_batch, label_batch, lambda r: None)
             return float(loss.d)
         if self.distributed:

@@ -210,20 +210,22 @@ def test_resnet18_cifar_step_vs_oracle(nnl, half):
     assert abs(got - want) <= (2e-2 if half else 1e-4) * max(1, abs(want))
     params = tr.models[0].trainable()
     assert set(params) == set(grads)
-    # Deep-chain tolerance, relative to each tensor's max: BN backward at 64
-    # elements/channel (4x4 maps, batch 4) amplifies summation-order differences
-    # (n*gy - sum(gy) - xhat*sum(gy*xhat)) layer after layer, and under Half every
-    # activation/gradient is re-rounded to fp16.  Conv biases feeding a train-mode
-    # BN have a mathematically zero gradient (pure rounding noise on both sides),
-    # hence the absolute floor relative to the largest gradient of the network.
-    gscale = max(np.abs(v.grad).max() for v in params.values())
-    floor = (1e-2 if half else 1e-3) * gscale
-    tol = 0.15 if half else 1e-2
+    # Normwise comparison.  Element-wise maxima are dominated by ReLU gates that
+    # flip where BN outputs sit within rounding distance of 0 (an integer decision
+    # taken on values that differ only by summation order: tools/debug_r18.py
+    # traces such a flip to one element of a stage-2 ReLU in fp32), while BN
+    # backward at 64 elements/channel amplifies summation-order differences.
+    # Conv biases feeding a train-mode BN have a mathematically zero gradient
+    # (rounding noise on both sides), hence the floor relative to the largest
+    # gradient norm of the network.
+    nrm = {k: np.linalg.norm(v.grad) for k, v in params.items()}
+    floor = (1e-2 if half else 1e-3) * max(nrm.values())
+    tol = 0.05 if half else 2e-3
     for k, v in params.items():
-        denom = max(np.abs(v.grad).max(), floor)
-        err = np.abs(grads[k] - v.grad).max() / denom
+        denom = max(nrm[k], floor)
+        err = np.linalg.norm(grads[k] - v.grad) / denom
         assert err < tol, (k, err)
         # w1 - w0 = -lr * g: the weight difference follows the gradient difference
-        ulp = 2.0 ** -10 * np.abs(v.value).max() if half else 0.0  # fp16 weight rounding
-        werr = np.abs(weights[k] - v.value).max() / (0.1 * denom + ulp)
-        assert werr < 1.5 * tol, (k, werr)
+        ulp = 2.0 ** -10 * np.linalg.norm(v.value) if half else 0.0  # fp16 weight rounding
+        werr = np.linalg.norm(weights[k] - v.value) / (0.1 * denom + ulp)
+        assert werr < 2 * tol, (k, werr)

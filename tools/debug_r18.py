@@ -49,3 +49,11 @@ for r in rows:
     if r[3] < 1e-4 or r[4] < 1e-6:
         continue
     print(f"{r[0]:22s} in{r[1]} {str(r[2]):22s} gerr {r[3]:.2e} (max {r[4]:.2e}) ferr {r[5]:.2e}")
+# normwise per-parameter errors (what tests/test_training_gpu.py checks)
+params = m.trainable()
+gpu = {k: v.g for k, v in reg.get_parameters().items()}
+nrm = {k: np.linalg.norm(v.grad) for k, v in params.items()}
+floor = (1e-2 if half else 1e-3) * max(nrm.values())
+errs = sorted(((np.linalg.norm(gpu[k] - v.grad) / max(nrm[k], floor), k)
+               for k, v in params.items()), reverse=True)
+print("normwise worst:", [(round(float(e), 5), k) for e, k in errs[:6]])
