@@ -14,6 +14,7 @@ the boundary with ``nnl_export_f32`` / ``nnl_import_f32``.
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 from enum import Enum
 
@@ -129,9 +130,11 @@ class NdArray:
         if src.shape != self.shape:
             raise ShapeMismatch(f"cannot write shape {src.shape} into {self.shape}")
         t = _lib.torch()
-        if not (src.flags.c_contiguous and src.flags.writeable):
+        if not src.flags.c_contiguous:
             src = np.array(src, dtype=np.float32, order="C")
-        host = t.from_numpy(src)
+        with warnings.catch_warnings():  # read-only views are only read here
+            warnings.simplefilter("ignore", UserWarning)
+            host = t.from_numpy(src)
         dev = host.to(self._t.device, non_blocking=host.is_pinned())
         self.write_f32_device(dev)
 

@@ -57,3 +57,13 @@ floor = (1e-2 if half else 1e-3) * max(nrm.values())
 errs = sorted(((np.linalg.norm(gpu[k] - v.grad) / max(nrm[k], floor), k)
                for k, v in params.items()), reverse=True)
 print("normwise worst:", [(round(float(e), 5), k) for e, k in errs[:6]])
+# noise floor: the same oracle on the batch in reversed order (identical math,
+# different summation order everywhere a reduction crosses the batch)
+m2 = O.Model(0, half)
+perm = np.arange(B)[::-1].copy()
+lo2 = m2.sce(O.resnet18_cifar(m2, O.Var(x[perm], half=half), 10), O.Var(lab[perm], half=half))
+O.backward(lo2, 8.0 if half else 1.0)
+p2 = m2.trainable()
+errs2 = sorted(((np.linalg.norm(p2[k].grad - v.grad) / max(nrm[k], floor), k)
+                for k, v in params.items()), reverse=True)
+print("oracle-vs-reordered-oracle worst:", [(round(float(e), 5), k) for e, k in errs2[:6]])
