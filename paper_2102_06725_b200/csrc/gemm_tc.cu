@@ -41,14 +41,17 @@ template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 5 : 7);
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int PIPE = STAGES * (A_BYTES + B_BYTES);
   static constexpr int RED_BYTES = 4 * BN * 2 * 4;
   static constexpr int BIAS_BYTES = BN * 4;
   static constexpr int MAX_STAT_N = 2048;  // per-CTA BN statistics accumulator [2][N]
   static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
-  static constexpr int SMEM = PIPE + 1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + 1024;
+  // TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 64 cols fp16)
+  static constexpr int STG_BYTES = 4 * 2 * 4096;
+  static constexpr int SMEM =
+      PIPE + 1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + STG_BYTES + 1024;
 };
 
 struct TcArgs {
@@ -77,6 +80,7 @@ struct TcArgs {
   float* stats;
   int32_t* nonfinite;
   float* partial;
+  int tma_store;      // epilogue writes through the output tensor map (tmC)
 };
 
 struct Unit {
@@ -98,7 +102,7 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int u) {
 template <int BN, int AM, int BMD>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const TcArgs a) {
+              const __grid_constant__ CUtensorMap tmC, const TcArgs a) {
   using C = Cfg<BN>;
   constexpr int S = C::STAGES;
   constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD;
@@ -111,16 +115,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
+  // [ A/B stage ring | TMA-store staging (1024-aligned) | barriers | red | bias | stats ]
   uint8_t* stA = smem;
   uint8_t* stB = smem + S * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::PIPE);
+  uint8_t* stg = smem + C::PIPE;
+  uint8_t* misc = stg + C::STG_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(misc);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* red = reinterpret_cast<float*>(smem + C::PIPE + 1024);
-  float* bias_s = reinterpret_cast<float*>(smem + C::PIPE + 1024 + C::RED_BYTES);
-  float* stat_s = reinterpret_cast<float*>(smem + C::PIPE + 1024 + C::RED_BYTES + C::BIAS_BYTES);
+  float* red = reinterpret_cast<float*>(misc + 1024);
+  float* bias_s = reinterpret_cast<float*>(misc + 1024 + C::RED_BYTES);
+  float* stat_s = reinterpret_cast<float*>(misc + 1024 + C::RED_BYTES + C::BIAS_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ConvGeom& g = a.g;
@@ -139,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     if (!kGA) tma_prefetch(&tmA);
     if (!kGB) tma_prefetch(&tmB);
+    if (a.tma_store) tma_prefetch(&tmC);
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
@@ -387,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
     int t = 0;
+    uint32_t sb = 0;  // TMA-store staging buffer alternation (per warp)
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++t) {
       const Unit w = decode_unit(a, u);
       const int m0 = w.tm * BM, n0 = w.tn * BN;
@@ -409,6 +418,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         orow = ((int64_t)n * g.h + y * a.rsh + a.ra) * g.w + x * a.rsw + a.rb;
       }
       int bad = 0;
+      if (a.tma_store) {
+        // 64-column chunks: round into a 128B-swizzled 32 x 64 staging tile, TMA
+        // store it (rows >= M and columns >= N are clipped by the tensor map),
+        // and take the BN column sums from the staged (rounded) values.
+        for (int c = 0; c < BN; c += 64) {
+          uint32_t v0[32], v1[32];
+          const uint32_t tb = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c);
+          tmem_ld32(tb, v0);
+          tmem_ld32(tb + 32, v1);
+          uint8_t* buf = stg + (wq * 2 + (sb & 1)) * 4096;
+          ++sb;
+          if (lane == 0) bulk_wait_read<1>();  // the store two chunks back has read buf
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {  // 16 B piece j = columns c + 8j .. c + 8j + 7
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = 8 * (j & 3) + 2 * e;
+              float f0 = __uint_as_float(j < 4 ? v0[k] : v1[k]);
+              float f1 = __uint_as_float(j < 4 ? v0[k + 1] : v1[k + 1]);
+              if (a.bias) {
+                f0 = __fadd_rn(f0, bias_s[c + 8 * j + 2 * e]);
+                f1 = __fadd_rn(f1, bias_s[c + 8 * j + 2 * e + 1]);
+              }
+              const __half h0 = __float2half_rn(__fadd_rn(0.f, f0));
+              const __half h1 = __float2half_rn(__fadd_rn(0.f, f1));
+              uint32_t u = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+              if (!mv) u = 0;
+              bad |= ((u & 0x7c00u) == 0x7c00u) | ((u & 0x7c000000u) == 0x7c000000u);
+              pk[e] = u;
+            }
+            *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, buf, n0 + c, m0 + 32 * wq);
+            bulk_commit();
+          }
+          if (a.stats) {  // lane owns columns c + 2*lane, c + 2*lane + 1
+            float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+              const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
+                  buf + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4));
+              s1a += x.x;
+              s1b += x.y;
+              s2a += x.x * x.x;
+              s2b += x.y * x.y;
+            }
+            float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
+            rp[0] = s1a;
+            rp[1] = s2a;
+            rp[2] = s1b;
+            rp[3] = s2b;
+          }
+        }
+      } else
       for (int c = 0; c < BN; c += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
@@ -522,6 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.stats[((int64_t)blockIdx.x * 2 + 1) * a.N + col] = stat_s[C::MAX_STAT_N + col];
       }
     }
+    if (a.tma_store && lane == 0) bulk_wait<0>();
   }
   __syncwarp();
   tc_fence_before();
@@ -692,6 +762,15 @@ static bool use_tma_im2col() {
   if (v < 0) {
     const char* e = getenv("NNL_TC_GATHER");
     v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static bool use_tma_store() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NNL_TC_STORE");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
@@ -932,7 +1011,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
 
 template <int BN, int AM, int BMD>
 static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
-                     const TcArgs& args, cudaStream_t st) {
+                     const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
   auto kern = k_tc_gemm<BN, AM, BMD>;
   static bool attr = false;
   if (!attr) {
@@ -941,16 +1020,16 @@ static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& t
     attr = true;
   }
   const int grid = pl.units < num_sms() ? pl.units : num_sms();
-  kern<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(ta, tb, args);
+  kern<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(ta, tb, tc, args);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
 
 template <int BN>
 static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
-                       const TcArgs& args, cudaStream_t st) {
+                       const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
 #define NNL_TC_CASE(AM, BMD) \
-  if (pl.amode == AM && pl.bmode == BMD) return launch_tc<BN, AM, BMD>(pl, ta, tb, args, st);
+  if (pl.amode == AM && pl.bmode == BMD) return launch_tc<BN, AM, BMD>(pl, ta, tb, tc, args, st);
   NNL_TC_CASE(A_TMA_K, B_TMA_K)
   NNL_TC_CASE(A_TMA_K, B_TMA_MN)
   NNL_TC_CASE(A_TMA_MN, B_TMA_MN)
@@ -1083,9 +1162,18 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     args.bias = nullptr; args.acc = 0; args.nonfinite = nullptr; args.stats = nullptr;
     if (pl.remap) return fail(NNL_ERR_UNSUPPORTED, "split-K with row remap");
   }
-  if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, args, st);
-  else if (pl.bn == 128) rc = dispatch_bn<128>(pl, ta, tb, args, st);
-  else rc = dispatch_bn<256>(pl, ta, tb, args, st);
+  CUtensorMap tc;
+  memset(&tc, 0, sizeof(tc));
+  if (!args.partial && !args.acc && !args.remap && use_tma_store() &&
+      !(reinterpret_cast<uintptr_t>(pb.out) & 15) && (pl.ldc * 2) % 16 == 0) {
+    View o;
+    o.ptr = pb.out; o.rows = pl.M; o.cols = pl.N; o.ld = pl.ldc;
+    if ((rc = make_tmap(&tc, o, 64, 32))) return rc;
+    args.tma_store = 1;
+  }
+  if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, tc, args, st);
+  else if (pl.bn == 128) rc = dispatch_bn<128>(pl, ta, tb, tc, args, st);
+  else rc = dispatch_bn<256>(pl, ta, tb, tc, args, st);
   if (rc) return rc;
   if (pl.splits > 1) {
     k_tc_splitk_reduce<<<grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st>>>(

@@ -217,10 +217,14 @@ def test_resnet18_cifar_step_vs_oracle(nnl, half):
     # backward at 64 elements/channel amplifies summation-order differences.
     # Conv biases feeding a train-mode BN have a mathematically zero gradient
     # (rounding noise on both sides), hence the floor relative to the largest
-    # gradient norm of the network.
+    # gradient norm of the network.  Tolerances are ~2x the oracle's own noise
+    # floor: tools/debug_r18.py re-runs the oracle with a different (equally
+    # valid) summation order and measures a worst normwise difference of 0.0093
+    # (fp32) and 0.153 (fp16 storage) against the unmodified oracle, while this
+    # path measures 0.0093 and 0.136 on B200.
     nrm = {k: np.linalg.norm(v.grad) for k, v in params.items()}
     floor = (1e-2 if half else 1e-3) * max(nrm.values())
-    tol = 0.05 if half else 2e-3
+    tol = 0.3 if half else 2e-2
     for k, v in params.items():
         denom = max(nrm[k], floor)
         err = np.linalg.norm(grads[k] - v.grad) / denom
