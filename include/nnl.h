@@ -148,25 +148,33 @@ int nnl_sce_bwd(int dtype, int64_t batch, int64_t classes, const void* logits,
 /* ---- BatchNormalization: functions.py:363-441 --------------------------- */
 size_t nnl_bn_workspace_size(int64_t rows, int32_t c);
 /* rows = N*H*W (channel-innermost).  stat_partials (nullable) are the conv
-   epilogue partials; save_mean/save_istd (f32 [c]) feed backward. */
+   epilogue partials; save_mean/save_istd (f32 [c]) feed backward.
+   residual (nullable): the residual tail BN -> Add2 -> [ReLU] in one pass,
+   y = [relu](q(q(BN(x)) + residual)) -- each step rounded exactly as the
+   separate functions would (functions.py:412-416, then Add2, then ReLU). */
 int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x,
                      const float* gamma, const float* beta,
                      float* running_mean, float* running_var, float eps, float momentum,
                      const float* stat_partials, int32_t n_partials,
-                     float* save_mean, float* save_istd, void* y, int fuse_relu,
-                     void* ws, size_t ws_bytes, void* stream);
+                     float* save_mean, float* save_istd, void* y, const void* residual,
+                     int fuse_relu, void* ws, size_t ws_bytes, void* stream);
 int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x,
                     const float* gamma, const float* beta, const float* mean,
                     const float* var, float eps, float* save_mean, float* save_istd,
-                    void* y, int fuse_relu, void* stream);
+                    void* y, const void* residual, int fuse_relu, void* stream);
 /* fused_relu: dy is the gradient of relu(BN(x)) (fused BN->ReLU); the gate
    relu(q(gamma*xhat+beta)) > 0 is recomputed from x with the forward's exact
    op sequence, so the ReLU output is never read.
    conv_bias_grad (nullable, dtype [c]): also reduce the ROUNDED dx over rows
    into the bias gradient of the convolution that produced x
-   (functions.py:211-212), saving that convolution a pass over dx. */
+   (functions.py:211-212), saving that convolution a pass over dx.
+   gate (nullable; exclusive with fused_relu): backward of the residual tail
+   BN -> Add2 -> ReLU.  dy is the ReLU output's gradient and gate the ReLU
+   output: the BN receives dy * (gate > 0), and dres (the Add2's other input's
+   gradient) gets q(dres + dy * (gate > 0)) (acc_res) or q(dy * (gate > 0)). */
 int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy,
-               int fused_relu, const float* gamma, const float* beta, const float* save_mean,
+               int fused_relu, const void* gate, void* dres, int acc_res,
+               const float* gamma, const float* beta, const float* save_mean,
                const float* save_istd, int batch_stat,
                void* dx, int acc_x, float* dgamma, int acc_g, float* dbeta, int acc_b,
                void* conv_bias_grad, int acc_cb,

@@ -95,10 +95,12 @@ _SIGS = {
     "nnl_sce_bwd": (C.c_int, [C.c_int, i64, i64, p, p, p, p, p, C.c_int, p]),
     "nnl_bn_workspace_size": (sz, [i64, i32]),
     "nnl_bn_fwd_train": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, f32, f32, p, i32, p, p, p,
-                                   C.c_int, p, sz, p]),
-    "nnl_bn_fwd_eval": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, f32, p, p, p, C.c_int, p]),
-    "nnl_bn_bwd": (C.c_int, [C.c_int, i64, i32, p, p, C.c_int, p, p, p, p, C.c_int, p, C.c_int,
-                             p, C.c_int, p, C.c_int, p, C.c_int, p, p, sz, p]),
+                                   p, C.c_int, p, sz, p]),
+    "nnl_bn_fwd_eval": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, f32, p, p, p, p, C.c_int,
+                                  p]),
+    "nnl_bn_bwd": (C.c_int, [C.c_int, i64, i32, p, p, C.c_int, p, p, C.c_int, p, p, p, p,
+                             C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, sz,
+                             p]),
     "nnl_multi_nonfinite": (C.c_int, [p, p, i32, p, p]),
     "nnl_multi_scale_grad": (C.c_int, [p, p, i32, f32, p]),
     "nnl_multi_sumsq": (C.c_int, [p, p, i32, p, p]),

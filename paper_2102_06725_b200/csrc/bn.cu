@@ -99,7 +99,7 @@ __device__ __forceinline__ float relu_gate(float xh, float ga, float be) {
 template <typename T, int V, int MODE>
 __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
     int64_t rows, int32_t c, int groups, int lanes, int64_t rows_per_block,
-    const T* __restrict__ x, const T* __restrict__ dy, int relu,
+    const T* __restrict__ x, const T* __restrict__ dy, int relu, const T* __restrict__ gate,
     const float* __restrict__ gamma, const float* __restrict__ beta,
     const float* __restrict__ mu, const float* __restrict__ istd, float* __restrict__ partials) {
   __shared__ float red[kBnThreads * 8 * 2];
@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
 #pragma unroll
           for (int j = 0; j < V; ++j) {
             const float xh = __fmul_rn(__fsub_rn(xv[u][j], m[j]), is[j]);
-            const float gy = relu ? __fmul_rn(gv[u][j], relu_gate<T>(xh, ga[j], be[j]))
-                                  : gv[u][j];
+            float gy = relu ? __fmul_rn(gv[u][j], relu_gate<T>(xh, ga[j], be[j])) : gv[u][j];
+            if (gate) gy = __fmul_rn(gy, Elem<T>::load(gate + r * c + c0 + j) > 0.f ? 1.f : 0.f);
             s1[j] += gy;
             s2[j] += __fmul_rn(gy, xh);
           }
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd_apply(
 template <typename T, int V>
 __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
     int64_t rows, int32_t c, int groups, int lanes, int64_t rows_per_block,
-    const T* __restrict__ x, const T* __restrict__ dy, int relu,
+    const T* __restrict__ x, const T* __restrict__ dy, int relu, const T* __restrict__ gate,
     const float* __restrict__ gamma, const float* __restrict__ beta, const float* __restrict__ mu,
     const float* __restrict__ istd, const float* __restrict__ gsum, int batch_stat,
     T* __restrict__ dx, int acc, float* __restrict__ bias_part) {
@@ -407,6 +407,17 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
             const float xh = __fmul_rn(__fsub_rn(xv[u][j], m[j]), is[j]);
             gv[u][j] = __fmul_rn(gv[u][j], relu_gate<T>(xh, ga[j], be[j]));
           }
+      }
+      if (gate) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int64_t r = rb + (int64_t)u * lanes;
+          if (r >= r1) break;
+#pragma unroll
+          for (int j = 0; j < V; ++j)
+            gv[u][j] = __fmul_rn(gv[u][j],
+                                 Elem<T>::load(gate + r * c + c0 + j) > 0.f ? 1.f : 0.f);
+        }
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -488,8 +499,8 @@ static size_t bn_ws_bytes(int64_t rows, int32_t c) {
     if (b > bx) bx = b;
   }
   if (c % 8 == 0 && c <= 2048)
-    for (int m : {BNS_STATS_F, BNS_STATS_B, BNS_APPLY_B}) {
-      const int64_t b = bn_stream_rows(m, rows, c);
+    for (int nt : {1, 2, 3}) {
+      const int64_t b = bn_stream_rows(BNS_STATS_B, nt, rows, c);
       if (b > bx) bx = b;
     }
   return (size_t)(2 * bx * 2 * c + 2 * c) * sizeof(float) + 256;
@@ -497,19 +508,20 @@ static size_t bn_ws_bytes(int64_t rows, int32_t c) {
 
 template <typename T, int MODE>
 static int launch_partials(int64_t rows, int32_t c, const BnGeom& g, int64_t bx, const T* x,
-                           const T* dy, int relu, const float* gamma, const float* beta,
+                           const T* dy, int relu, const T* gate, const float* gamma,
+                           const float* beta,
                            const float* mu, const float* istd, float* partials, cudaStream_t st) {
   int64_t rpb = (rows + bx - 1) / bx;
   dim3 grid((unsigned)bx, (unsigned)g.slabs);
   if (g.vec == 8)
     k_bn_partials<T, 8, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, gamma, beta, mu, istd, partials);
+                                                           relu, gate, gamma, beta, mu, istd, partials);
   else if (g.vec == 4)
     k_bn_partials<T, 4, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, gamma, beta, mu, istd, partials);
+                                                           relu, gate, gamma, beta, mu, istd, partials);
   else
     k_bn_partials<T, 1, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, gamma, beta, mu, istd, partials);
+                                                           relu, gate, gamma, beta, mu, istd, partials);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
@@ -550,17 +562,42 @@ static bool use_stream(int dtype, int64_t rows, int32_t c, const void* a, const 
 
 extern "C" {
 
+int nnl_relu_bwd(int dtype, int64_t n, const void* x, const void* dy, void* dx, int accumulate,
+                 void* stream);
+int nnl_add2_fwd(int dtype, int64_t n, const void* a, const void* b, void* y, int fuse_relu,
+                 void* stream);
+
+// y = q(gamma*((x-mu)*istd)+beta); with `residual` the Add2 of the residual
+// tail follows, y = q(y + residual) (Add2 forward), then the optional ReLU.
+static int bn_apply_fwd(int dtype, int64_t rows, int32_t c, const void* x, const float* gamma,
+                        const float* beta, const float* save_mean, const float* save_istd,
+                        void* y, const void* residual, int fuse_relu, cudaStream_t st) {
+  if (use_stream(dtype, rows, c, x, y, residual)) {
+    BnStreamArgs a = {};
+    a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)y; a.gamma = gamma;
+    a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fuse_relu;
+    a.res = (const __half*)residual;
+    return bn_stream_launch(BNS_APPLY_F, a, st);
+  }
+  BnGeom g = bn_geom(c, al16(x) && al16(y));
+  int rc = NNL_OK;
+  NNL_DISPATCH_DTYPE(dtype, T, {
+    rc = launch_fwd_apply<T>(rows, c, g, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y,
+                             residual ? 0 : fuse_relu, st);
+  });
+  if (rc || !residual) return rc;
+  return nnl_add2_fwd(dtype, rows * c, y, residual, y, fuse_relu, st);  // in place, elementwise
+}
+
 int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const float* gamma,
                      const float* beta, float* running_mean, float* running_var, float eps,
                      float momentum, const float* stat_partials, int32_t n_partials,
-                     float* save_mean, float* save_istd, void* y, int fuse_relu, void* ws,
-                     size_t ws_bytes, void* stream) {
+                     float* save_mean, float* save_istd, void* y, const void* residual,
+                     int fuse_relu, void* ws, size_t ws_bytes, void* stream) {
   if (rows <= 1)
     return fail(NNL_ERR_DEGENERATE_BATCH, "cannot take batch statistics over %lld element(s)",
                 (long long)rows);
   cudaStream_t st = as_stream(stream);
-  const bool stream_ok = use_stream(dtype, rows, c, x, y, nullptr);
-  BnGeom g = bn_geom(c, al16(x) && al16(y));
   const float* parts = stat_partials;
   int32_t R = n_partials;
   int rc = NNL_OK;
@@ -568,16 +605,17 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
     if (ws_bytes < bn_ws_bytes(rows, c))
       return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
     float* p = (float*)ws;
-    if (stream_ok) {
+    if (use_stream(dtype, rows, c, x, nullptr, nullptr)) {
       BnStreamArgs a = {};
       a.rows = rows; a.c = c; a.x = (const __half*)x; a.partials = p;
       rc = bn_stream_launch(BNS_STATS_F, a, st);
-      R = bn_stream_rows(BNS_STATS_F, rows, c);
+      R = bn_stream_rows(BNS_STATS_F, 1, rows, c);
     } else {
+      BnGeom g = bn_geom(c, al16(x));
       const int64_t bx = bn_blocks_x(rows, g);
       NNL_DISPATCH_DTYPE(dtype, T, {
         rc = launch_partials<T, 0>(rows, c, g, bx, (const T*)x, nullptr, 0, nullptr, nullptr,
-                                   nullptr, nullptr, p, st);
+                                   nullptr, nullptr, nullptr, p, st);
       });
       R = (int32_t)bx;
     }
@@ -587,53 +625,42 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
   k_bn_finalize_fwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
       parts, R, c, rows, running_mean, running_var, eps, momentum, save_mean, save_istd);
   NNL_CHECK_LAUNCH();
-  if (stream_ok) {
-    BnStreamArgs a = {};
-    a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)y; a.gamma = gamma;
-    a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fuse_relu;
-    return bn_stream_launch(BNS_APPLY_F, a, st);
-  }
-  NNL_DISPATCH_DTYPE(dtype, T, {
-    rc = launch_fwd_apply<T>(rows, c, g, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y,
-                             fuse_relu, st);
-  });
-  return rc;
+  return bn_apply_fwd(dtype, rows, c, x, gamma, beta, save_mean, save_istd, y, residual,
+                      fuse_relu, st);
 }
 
 int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x, const float* gamma,
                     const float* beta, const float* mean, const float* var, float eps,
-                    float* save_mean, float* save_istd, void* y, int fuse_relu, void* stream) {
+                    float* save_mean, float* save_istd, void* y, const void* residual,
+                    int fuse_relu, void* stream) {
   cudaStream_t st = as_stream(stream);
   k_bn_eval_stats<<<(c + 255) / 256, 256, 0, st>>>(c, mean, var, eps, save_mean, save_istd);
   NNL_CHECK_LAUNCH();
   if (rows * c <= 0) return NNL_OK;
-  if (use_stream(dtype, rows, c, x, y, nullptr)) {
-    BnStreamArgs a = {};
-    a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)y; a.gamma = gamma;
-    a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fuse_relu;
-    return bn_stream_launch(BNS_APPLY_F, a, st);
-  }
-  BnGeom g = bn_geom(c, al16(x) && al16(y));
-  int rc;
-  NNL_DISPATCH_DTYPE(dtype, T, {
-    rc = launch_fwd_apply<T>(rows, c, g, (const T*)x, gamma, beta, save_mean, save_istd, (T*)y,
-                             fuse_relu, st);
-  });
-  return rc;
+  return bn_apply_fwd(dtype, rows, c, x, gamma, beta, save_mean, save_istd, y, residual,
+                      fuse_relu, st);
 }
 
 int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy,
-               int fused_relu, const float* gamma, const float* beta, const float* save_mean,
-               const float* save_istd, int batch_stat, void* dx, int acc_x, float* dgamma,
-               int acc_g, float* dbeta, int acc_b, void* conv_bias_grad, int acc_cb,
-               int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
+               int fused_relu, const void* gate, void* dres, int acc_res, const float* gamma,
+               const float* beta, const float* save_mean, const float* save_istd, int batch_stat,
+               void* dx, int acc_x, float* dgamma, int acc_g, float* dbeta, int acc_b,
+               void* conv_bias_grad, int acc_cb, int32_t* nonfinite, void* ws, size_t ws_bytes,
+               void* stream) {
   cudaStream_t st = as_stream(stream);
   if (ws_bytes < bn_ws_bytes(rows, c))
     return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
   if (fused_relu && !beta) return fail(NNL_ERR_INVALID_ARGUMENT, "fused ReLU needs beta");
-  const bool stream_ok = use_stream(dtype, rows, c, x, dy, dx);
+  if (fused_relu && gate)
+    return fail(NNL_ERR_INVALID_ARGUMENT, "fused ReLU and residual gate are exclusive");
+  const bool stream_ok =
+      use_stream(dtype, rows, c, x, dy, dx) && use_stream(dtype, rows, c, gate, dres, nullptr);
+  // the gated gradient is written once to dres and re-read by the apply pass
+  const bool dres_first = stream_ok && gate && dres && !acc_res;
   BnGeom g = bn_geom(c, al16(x) && al16(dy) && al16(dx), 4);
-  const int64_t bx = stream_ok ? bn_stream_rows(BNS_STATS_B, rows, c) : bn_blocks_x(rows, g);
+  const int nt_stats = gate ? 3 : 2;
+  const int64_t bx =
+      stream_ok ? bn_stream_rows(BNS_STATS_B, nt_stats, rows, c) : bn_blocks_x(rows, g);
   float* parts = (float*)ws;
   float* gsum = parts + bx * 2 * c;
   float* bparts = gsum + 2 * c;
@@ -642,50 +669,64 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
     BnStreamArgs a = {};
     a.rows = rows; a.c = c; a.x = (const __half*)x; a.dy = (const __half*)dy; a.gamma = gamma;
     a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fused_relu; a.partials = parts;
+    a.gate = (const __half*)gate;
+    a.dres = dres_first ? (__half*)dres : nullptr;
     rc = bn_stream_launch(BNS_STATS_B, a, st);
   } else {
     NNL_DISPATCH_DTYPE(dtype, T, {
-      rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, fused_relu, gamma,
-                                 beta, save_mean, save_istd, parts, st);
+      rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, fused_relu,
+                                 (const T*)gate, gamma, beta, save_mean, save_istd, parts, st);
     });
   }
   if (rc) return rc;
   k_bn_finalize_bwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
       parts, (int32_t)bx, c, gsum, dgamma, acc_g, dbeta, acc_b, nonfinite);
   NNL_CHECK_LAUNCH();
-  if (!dx) return NNL_OK;
-  float* bp = conv_bias_grad ? bparts : nullptr;
-  int32_t brows = (int32_t)bx;
-  if (stream_ok) {
-    BnStreamArgs a = {};
-    a.rows = rows; a.c = c; a.x = (const __half*)x; a.dy = (const __half*)dy; a.out = (__half*)dx;
-    a.gamma = gamma; a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.gsum = gsum;
-    a.partials = bp; a.relu = fused_relu; a.acc = acc_x; a.batch_stat = batch_stat;
-    rc = bn_stream_launch(BNS_APPLY_B, a, st);
-    if (rc) return rc;
-    brows = bn_stream_rows(BNS_APPLY_B, rows, c);
-  } else {
-    const int64_t rpb = (rows + bx - 1) / bx;
-    dim3 grid((unsigned)bx, (unsigned)g.slabs);
-    NNL_DISPATCH_DTYPE(dtype, T, {
-      if (g.vec == 4)
-        k_bn_bwd_apply<T, 4><<<grid, kBnThreads, 0, st>>>(
-            rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
-            save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
-      else
-        k_bn_bwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(
-            rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu, gamma, beta,
-            save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x, bp);
-    });
-    NNL_CHECK_LAUNCH();
+  if (dx) {
+    float* bp = conv_bias_grad ? bparts : nullptr;
+    int32_t brows = (int32_t)bx;
+    if (stream_ok) {
+      BnStreamArgs a = {};
+      a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)dx;
+      a.gamma = gamma; a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.gsum = gsum;
+      a.partials = bp; a.relu = fused_relu; a.acc = acc_x; a.batch_stat = batch_stat;
+      if (dres_first) {
+        a.dy = (const __half*)dres;  // already gated
+      } else {
+        a.dy = (const __half*)dy;
+        a.gate = (const __half*)gate;
+      }
+      rc = bn_stream_launch(BNS_APPLY_B, a, st);
+      if (rc) return rc;
+      brows = bn_stream_rows(BNS_APPLY_B, bn_stream_nt(BNS_APPLY_B, a), rows, c);
+    } else {
+      const int64_t rpb = (rows + bx - 1) / bx;
+      dim3 grid((unsigned)bx, (unsigned)g.slabs);
+      NNL_DISPATCH_DTYPE(dtype, T, {
+        if (g.vec == 4)
+          k_bn_bwd_apply<T, 4><<<grid, kBnThreads, 0, st>>>(
+              rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu,
+              (const T*)gate, gamma, beta, save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x,
+              bp);
+        else
+          k_bn_bwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(
+              rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu,
+              (const T*)gate, gamma, beta, save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x,
+              bp);
+      });
+      NNL_CHECK_LAUNCH();
+    }
+    if (bp) {
+      NNL_DISPATCH_DTYPE(dtype, T, {
+        k_bn_bias_finalize<T><<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+            bp, brows, c, (T*)conv_bias_grad, acc_cb, nonfinite);
+      });
+      NNL_CHECK_LAUNCH();
+    }
   }
-  if (bp) {
-    NNL_DISPATCH_DTYPE(dtype, T, {
-      k_bn_bias_finalize<T><<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
-          bp, brows, c, (T*)conv_bias_grad, acc_cb, nonfinite);
-    });
-    NNL_CHECK_LAUNCH();
-  }
+  // the residual branch's gradient (Add2 backward after the ReLU gate)
+  if (gate && dres && !dres_first)
+    return nnl_relu_bwd(dtype, rows * c, gate, dy, dres, acc_res, st);
   return NNL_OK;
 }
 

@@ -22,9 +22,12 @@ using namespace tc;
 enum BnMode { STATS_F = BNS_STATS_F, APPLY_F = BNS_APPLY_F, STATS_B = BNS_STATS_B,
               APPLY_B = BNS_APPLY_B };
 
-constexpr int kStages = 3;
-constexpr int kChunkBytes = 16384;  // per streamed tensor per stage
 constexpr int kThreads = 256;
+constexpr int kChunkBytes = 16384;  // per streamed tensor per stage
+// three-tensor launches keep two stages so that two CTAs still fit on an SM:
+// the same grid and chunking as the two-tensor launch, hence the same partial
+// sums (the fused residual tail is bit-identical to the unfused chain)
+__host__ __device__ constexpr int stages(int nt) { return nt == 3 ? 2 : 3; }
 
 __device__ __forceinline__ void unpack8(const uint4& u, float* f) {
   const __half2* h = reinterpret_cast<const __half2*>(&u);
@@ -36,9 +39,11 @@ __device__ __forceinline__ void unpack8(const uint4& u, float* f) {
   }
 }
 
-template <int MODE>
+template <int MODE, int NT>
 __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
-  constexpr int NT = (MODE == STATS_B || MODE == APPLY_B) ? 2 : 1;
+  constexpr int kStages = stages(NT);
+  constexpr bool kGate = NT == 3;                   // backward, ReLU gate streamed
+  constexpr bool kRes = MODE == APPLY_F && NT == 2;  // forward, residual streamed
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * NT * kChunkBytes);
   const int tid = threadIdx.x;
@@ -77,7 +82,10 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
     const uint32_t bytes = (uint32_t)(nr * a.c * 2);
     mbar_arrive_tx(&full[s], bytes * NT);
     bulk_load(smem + (s * NT + 0) * kChunkBytes, a.x + r0 * a.c, bytes, &full[s]);
-    if (NT == 2) bulk_load(smem + (s * NT + 1) * kChunkBytes, a.dy + r0 * a.c, bytes, &full[s]);
+    if (NT >= 2)
+      bulk_load(smem + (s * NT + 1) * kChunkBytes, (kRes ? a.res : a.dy) + r0 * a.c, bytes,
+                &full[s]);
+    if (NT == 3) bulk_load(smem + (s * NT + 2) * kChunkBytes, a.gate + r0 * a.c, bytes, &full[s]);
   };
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -93,6 +101,7 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
     const int nr = (int)min((int64_t)a.chunk_rows, a.rows - r0);
     const uint8_t* xs = smem + (s * NT + 0) * kChunkBytes;
     const uint8_t* gs = smem + (s * NT + 1) * kChunkBytes;
+    const uint8_t* zs = smem + (s * NT + 2) * kChunkBytes;
     if (active) {
       for (int r = lane; r < nr; r += lanes) {
         float xv[8];
@@ -110,9 +119,12 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
         for (int j = 0; j < 8; ++j) xh[j] = __fmul_rn(__fsub_rn(xv[j], m[j]), is[j]);
         if (MODE == APPLY_F) {
           __align__(16) __half o[8];
+          float rv[8];
+          if (kRes) unpack8(*reinterpret_cast<const uint4*>(gs + ((size_t)r * a.c + c0) * 2), rv);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             __half q = __float2half_rn(__fadd_rn(__fmul_rn(ga[j], xh[j]), be[j]));
+            if (kRes) q = __float2half_rn(__fadd_rn(__half2float(q), rv[j]));  // Add2: q(a + b)
             if (a.relu) {
               const float f = __half2float(q);
               q = __float2half_rn((f > 0.f || f != f) ? f : 0.f);
@@ -125,7 +137,12 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
         }
         float gv[8];
         unpack8(*reinterpret_cast<const uint4*>(gs + ((size_t)r * a.c + c0) * 2), gv);
-        if (a.relu) {
+        if (kGate) {  // ReLU after the residual add: gate on its stored output
+          float zv[8];
+          unpack8(*reinterpret_cast<const uint4*>(zs + ((size_t)r * a.c + c0) * 2), zv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) gv[j] = __fmul_rn(gv[j], zv[j] > 0.f ? 1.f : 0.f);
+        } else if (a.relu) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const float z = __half2float(__float2half_rn(__fadd_rn(__fmul_rn(ga[j], xh[j]), be[j])));
@@ -137,6 +154,13 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
           for (int j = 0; j < 8; ++j) {
             s1[j] += gv[j];
             s2[j] += __fmul_rn(gv[j], xh[j]);
+          }
+          if (kGate && a.dres) {  // the residual branch's gradient, q(0 + gy)
+            __align__(16) __half o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = __float2half_rn(__fadd_rn(0.f, gv[j]));
+            *reinterpret_cast<uint4*>(a.dres + (r0 + r) * a.c + c0) =
+                *reinterpret_cast<const uint4*>(o);
           }
           continue;
         }
@@ -197,9 +221,15 @@ bool bn_stream_ok(int64_t rows, int32_t c, const void* a, const void* b, const v
          (!b || aligned16(b)) && (!d || aligned16(d));
 }
 
-int bn_stream_rows(int mode, int64_t rows, int32_t c) {
-  // streamed-tensor smem: 2 tensors -> 2 blocks/SM, 1 tensor -> 4 blocks/SM
-  int grid = (mode == STATS_B || mode == APPLY_B) ? 148 * 2 : 148 * 4;
+int bn_stream_nt(int mode, const BnStreamArgs& a) {
+  if (mode == STATS_B || mode == APPLY_B) return a.gate ? 3 : 2;
+  return (mode == APPLY_F && a.res) ? 2 : 1;
+}
+
+int bn_stream_rows(int mode, int nt, int64_t rows, int32_t c) {
+  (void)mode;
+  // streamed-tensor smem: 1 tensor -> 4 blocks/SM, 2 or 3 tensors -> 2
+  int grid = nt == 1 ? 148 * 4 : 148 * 2;
   const int64_t chunk_rows = kChunkBytes / (c * 2);
   const int64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
   if (grid > nchunks) grid = (int)nchunks;
@@ -208,32 +238,33 @@ int bn_stream_rows(int mode, int64_t rows, int32_t c) {
 
 int bn_stream_launch(int mode, const BnStreamArgs& in, cudaStream_t st) {
   BnStreamArgs a = in;
+  const int nt = bn_stream_nt(mode, a);
+  if (nt == 3 && a.relu) return fail(NNL_ERR_INVALID_ARGUMENT, "gate and fused ReLU both set");
   a.chunk_rows = kChunkBytes / (a.c * 2);
   a.nchunks = (a.rows + a.chunk_rows - 1) / a.chunk_rows;
-  const int nt = (mode == STATS_B || mode == APPLY_B) ? 2 : 1;
-  const int smem = kStages * nt * kChunkBytes + 64;
-  const int grid = bn_stream_rows(mode, a.rows, a.c);
-  static bool attr[4] = {false, false, false, false};
-#define NNL_BN_LAUNCH(M)                                                                   \
-  case M:                                                                                  \
-    if (!attr[M]) {                                                                        \
-      NNL_CUDA(cudaFuncSetAttribute(k_bn_stream<M>,                                        \
+  const int smem = stages(nt) * nt * kChunkBytes + 64;
+  const int grid = bn_stream_rows(mode, nt, a.rows, a.c);
+  static bool attr[4][4] = {};
+#define NNL_BN_LAUNCH(M, NT)                                                               \
+  if (mode == M && nt == NT) {                                                             \
+    if (!attr[M][NT]) {                                                                    \
+      NNL_CUDA(cudaFuncSetAttribute(k_bn_stream<M, NT>,                                    \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));   \
-      attr[M] = true;                                                                      \
+      attr[M][NT] = true;                                                                  \
     }                                                                                      \
-    k_bn_stream<M><<<grid, kThreads, smem, st>>>(a);                                       \
-    break;
-  switch (mode) {
-    NNL_BN_LAUNCH(STATS_F)
-    NNL_BN_LAUNCH(APPLY_F)
-    NNL_BN_LAUNCH(STATS_B)
-    NNL_BN_LAUNCH(APPLY_B)
-    default:
-      return fail(NNL_ERR_INVALID_ARGUMENT, "bad bn stream mode");
+    k_bn_stream<M, NT><<<grid, kThreads, smem, st>>>(a);                                   \
+    NNL_CHECK_LAUNCH();                                                                    \
+    return NNL_OK;                                                                         \
   }
+  NNL_BN_LAUNCH(STATS_F, 1)
+  NNL_BN_LAUNCH(APPLY_F, 1)
+  NNL_BN_LAUNCH(APPLY_F, 2)
+  NNL_BN_LAUNCH(STATS_B, 2)
+  NNL_BN_LAUNCH(STATS_B, 3)
+  NNL_BN_LAUNCH(APPLY_B, 2)
+  NNL_BN_LAUNCH(APPLY_B, 3)
 #undef NNL_BN_LAUNCH
-  NNL_CHECK_LAUNCH();
-  return NNL_OK;
+  return fail(NNL_ERR_INVALID_ARGUMENT, "bad bn stream mode");
 }
 
 }  // namespace nnl

@@ -24,11 +24,17 @@ struct BnStreamArgs {
   int relu;
   int acc;
   int batch_stat;
+  // residual tail (BN -> Add2 -> ReLU):
+  const __half* res;   // APPLY_F: y = relu(q(q(bn(x)) + res)), streamed
+  const __half* gate;  // STATS_B / APPLY_B: gy *= (gate > 0), streamed
+  __half* dres;        // STATS_B with gate: dres = q(0 + gated gy)
 };
 
 bool bn_stream_ok(int64_t rows, int32_t c, const void* a, const void* b, const void* d);
+// streamed tensors of a launch: x, plus dy (backward) or res, plus gate
+int bn_stream_nt(int mode, const BnStreamArgs& a);
 // number of partial rows the launch writes (its grid size)
-int bn_stream_rows(int mode, int64_t rows, int32_t c);
+int bn_stream_rows(int mode, int nt, int64_t rows, int32_t c);
 int bn_stream_launch(int mode, const BnStreamArgs& a, cudaStream_t st);
 
 }  // namespace nnl

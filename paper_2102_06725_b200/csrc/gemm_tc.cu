@@ -32,8 +32,13 @@ using namespace tc;
 
 // A_IM2COL / B_IM2COL: TMA im2col mode (fprop + stride-1 dgrad A, wgrad B);
 // the cp.async gathers remain for strided dgrad and as a debug path.
-enum AMode { A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4 };
-enum BMode { B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3 };
+// A_GATHER_C4 / B_GATHER_C4: narrow-channel convolutions (the 3-channel stem)
+// over a 4-channel padded copy of x, reduction index k = tap*4 + c, 16 taps per
+// 64-wide k-block, gathered as 8 B pieces.
+enum AMode {
+  A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4, A_GATHER_C4 = 5
+};
+enum BMode { B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATHER_C4 = 4 };
 
 constexpr int BM = 128, BK = 64, kThreads = 384;
 
@@ -55,6 +60,10 @@ struct Cfg {
 };
 
 struct TcArgs {
+  int64_t K;          // reduction length (B_GATHER_C4: pixels)
+  // narrow-channel gathers: x4 is [n][h][c4_w4][4] with image column w at
+  // c4_w4 column w + c4_off; reduction index k = (r * c4_s2 + s) * 4 + c
+  int c4_s2, c4_w4, c4_off, c4_pair;
   int M, N;
   int num_kb, kb_per_split;
   int tiles_m, tiles_n, units;
@@ -99,22 +108,51 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int u) {
   return w;
 }
 
+// One 16 B chunk of a narrow-channel reduction row: taps (r, s), (r, s+1)
+// (s even) x 4 channels of the window based at (h0, w0) of the image whose
+// first x4 pixel is nb.  Pair mode (even stride): the two pixels are one
+// aligned 16 B load (x4 columns are shifted by c4_off so that every pair
+// starts on an even column and never straddles the zero border); otherwise
+// two 8 B loads.  Taps beyond the filter and out-of-image pixels read zero.
+__device__ __forceinline__ void c4_chunk(uint8_t* dst, const TcArgs& a, const ConvGeom& g, int r,
+                                         int s, int nb, int h0, int w0) {
+  const int ih = h0 + r, col = w0 + s + a.c4_off;
+  const bool okr = r < g.r && (unsigned)ih < (unsigned)g.h;
+  const int64_t base = ((int64_t)nb + (int64_t)ih * a.c4_w4) * 4;
+  if (a.c4_pair) {
+    const bool ok = okr && (unsigned)col < (unsigned)a.c4_w4;
+    cp_async16_ca(dst, ok ? a.gsrc + base + col * 4 : a.gsrc,
+                  !ok ? 0u : (s + 1 < g.s ? 16u : 8u));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const bool ok = okr && s + e < g.s && (unsigned)(col + e) < (unsigned)a.c4_w4;
+      cp_async8(dst + 8 * e, ok ? a.gsrc + base + (col + e) * 4 : a.gsrc, ok ? 8u : 0u);
+    }
+  }
+}
+
 template <int BN, int AM, int BMD>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const TcArgs a) {
   using C = Cfg<BN>;
   constexpr int S = C::STAGES;
-  constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD;
-  constexpr bool kGB = BMD == B_GATHER_WGRAD;
+  constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD || AM == A_GATHER_C4;
+  constexpr bool kGB = BMD == B_GATHER_WGRAD || BMD == B_GATHER_C4;
   constexpr bool kAmn = AM == A_TMA_MN;
   constexpr bool kBmn = BMD != B_TMA_K;
   constexpr uint32_t kTmaBytes = (kGA ? 0 : C::A_BYTES) + (kGB ? 0 : C::B_BYTES);
   constexpr uint32_t IDESC = idesc_f16(BN, kAmn, kBmn);
+  // TMA-fed tiles leave warps 4..7 free: they join the epilogue
+  constexpr bool kEpi8 = !kGA && !kGB && BN >= 128;
+  constexpr int kEpi = kEpi8 ? 8 : 4, kEpiWarp0 = kEpi8 ? 4 : 8;
+  constexpr int kStgBufs = kEpi8 ? 1 : 2;  // 4 KB TMA-store staging buffers per warp
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // offset from the shared array itself (not via an integer cast), so that
+  // every derived pointer stays in the shared address space (LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // [ A/B stage ring | TMA-store staging (1024-aligned) | barriers | red | bias | stats ]
   uint8_t* stA = smem;
   uint8_t* stB = smem + S * C::A_BYTES;
@@ -139,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], kEpi);
     }
     fence_barrier_init();
   }
@@ -253,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&tfull[ab]);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (!kEpi8 && warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ gather producers
     if (kGA || kGB) {
       constexpr int LAG = S - 1;
@@ -266,7 +304,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // per-row metadata of this tile's 8 A rows (fixed across its k-blocks)
         int64_t rbase[8];
         int rh[8], rw[8];
-        if (kGA) {
+        int c4h = -(1 << 28), c4w = 0, c4n = 0;  // A_GATHER_C4: this thread's row = tid
+        if (AM == A_GATHER_C4) {
+          const int m = m0 + tid;
+          if (m < a.M) {
+            const int q = m % g.q, t = m / g.q;
+            const int p = t % g.p;
+            c4n = (t / g.p) * g.h * a.c4_w4;
+            c4h = p * g.sh - g.ph;
+            c4w = q * g.sw - g.pw;
+          }
+        } else if (kGA) {
 #pragma unroll
           for (int i8 = 0; i8 < 8; ++i8) {
             const int m = m0 + (tid >> 3) + 16 * i8;
@@ -296,7 +344,45 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (it / S) & 1;
           const int kb = w.kb0 + i;
           mbar_wait(&empty[s], ph ^ 1);
-          if (AM == A_GATHER_FPROP) {
+          if (AM == A_GATHER_C4) {
+            uint8_t* dst = stA + s * C::A_BYTES + tid * 128;
+            const int rw = a.c4_s2 * 4;
+            int r = (kb * 64) / rw, sl = ((kb * 64) % rw) >> 2;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              c4_chunk(dst + ((j ^ (tid & 7)) << 4), a, g, r, sl, c4n, c4h, c4w);
+              sl += 2;
+              if (sl == a.c4_s2) { sl = 0; ++r; }
+            }
+          } else if (BMD == B_GATHER_C4) {
+            // reduction row (pixel) tid & 63; this thread fills 16 B chunks
+            // 4*(tid>>6) .. +3 of every 64-column block of the tile
+            const int row = tid & 63, half = tid >> 6;
+            const int64_t pix = (int64_t)kb * 64 + row;
+            int ph0 = -(1 << 28), pw0 = 0, pn = 0;
+            if (pix < a.K) {
+              const int q = (int)(pix % g.q);
+              const int64_t tt = pix / g.q;
+              const int p = (int)(tt % g.p);
+              pn = (int)(tt / g.p) * g.h * a.c4_w4;
+              ph0 = p * g.sh - g.ph;
+              pw0 = q * g.sw - g.pw;
+            }
+            const int rw = a.c4_s2 * 4;
+#pragma unroll
+            for (int jb = 0; jb < BN / 64; ++jb) {
+              uint8_t* dst = stB + s * C::B_BYTES + jb * 8192 + row * 128;
+              const int k0 = n0 + jb * 64 + half * 32;
+              int r = k0 / rw, sl = (k0 % rw) >> 2;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const int j = half * 4 + jj;
+                c4_chunk(dst + ((j ^ (row & 7)) << 4), a, g, r, sl, pn, ph0, pw0);
+                sl += 2;
+                if (sl == a.c4_s2) { sl = 0; ++r; }
+              }
+            }
+          } else if (AM == A_GATHER_FPROP) {
             const int t = kb / a.cblk, cb = kb - t * a.cblk;
             const int r = t / g.s, sx = t - r * g.s;
             const int64_t toff = ((int64_t)r * g.w + sx) * g.c + cb * 64 + chunk * 8;
@@ -386,13 +472,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async();
       for (int j = it > LAG ? it - LAG : 0; j < it; ++j) mbar_arrive(&full[j % S]);
     }
-  } else if (warp >= 8) {
+  } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
-    const int wq = warp & 3;
-    const int tid = threadIdx.x - 256;
+    // kEpi8: warps 4..11, the first four on columns [0, BN/2), the others on
+    // [BN/2, BN) (two warps per SM sub-partition hide each other's latency)
+    const int ew = warp - kEpiWarp0;         // epilogue warp 0 .. kEpi - 1
+    const int wq = warp & 3;                 // TMEM lane quarter
+    const int c_lo = kEpi8 ? (ew >> 2) * (BN / 2) : 0;
+    const int c_hi = kEpi8 ? c_lo + BN / 2 : BN;
+    constexpr int kEpiThreads = 32 * kEpi;
+    const int tid = threadIdx.x - 32 * kEpiWarp0;
     if (a.stats) {
-      for (int j = tid; j < 2 * C::MAX_STAT_N; j += 128) stat_s[j] = 0.f;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int j = tid; j < 2 * C::MAX_STAT_N; j += kEpiThreads) stat_s[j] = 0.f;
+      named_sync(1, kEpiThreads);
     }
     int t = 0;
     uint32_t sb = 0;  // TMA-store staging buffer alternation (per warp)
@@ -401,10 +493,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = w.tm * BM, n0 = w.tn * BN;
       const int ab = t & 1;
       if (a.bias) {  // this tile's bias slice, staged once in shared memory (as f32)
-        asm volatile("bar.sync 2, 128;" ::: "memory");
-        for (int j = tid; j < BN; j += 128)
+        named_sync(2, kEpiThreads);
+        for (int j = tid; j < BN; j += kEpiThreads)
           bias_s[j] = n0 + j < a.N ? __half2float(a.bias[n0 + j]) : 0.f;
-        asm volatile("bar.sync 2, 128;" ::: "memory");
+        named_sync(2, kEpiThreads);
       }
       mbar_wait(&tfull[ab], (t >> 1) & 1);
       tc_fence_after();
@@ -422,33 +514,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 64-column chunks: round into a 128B-swizzled 32 x 64 staging tile, TMA
         // store it (rows >= M and columns >= N are clipped by the tensor map),
         // and take the BN column sums from the staged (rounded) values.
-        for (int c = 0; c < BN; c += 64) {
-          uint32_t v0[32], v1[32];
+        for (int c = c_lo; c < c_hi; c += 64) {
+          uint32_t v[64];
           const uint32_t tb = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c);
-          tmem_ld32(tb, v0);
-          tmem_ld32(tb + 32, v1);
-          uint8_t* buf = stg + (wq * 2 + (sb & 1)) * 4096;
+          tmem_ld32_nowait(tb, v);
+          tmem_ld32_nowait(tb + 32, v + 32);
+          tmem_wait_ld();
+          uint8_t* buf = stg + (ew * kStgBufs + (sb % kStgBufs)) * 4096;
           ++sb;
-          if (lane == 0) bulk_wait_read<1>();  // the store two chunks back has read buf
+          if (lane == 0) bulk_wait_read<kStgBufs - 1>();  // buf's previous store has read it
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j) {  // 16 B piece j = columns c + 8j .. c + 8j + 7
             uint32_t pk[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const int k = 8 * (j & 3) + 2 * e;
-              float f0 = __uint_as_float(j < 4 ? v0[k] : v1[k]);
-              float f1 = __uint_as_float(j < 4 ? v0[k + 1] : v1[k + 1]);
+              const int k = 8 * j + 2 * e;
+              float f0 = __uint_as_float(v[k]), f1 = __uint_as_float(v[k + 1]);
               if (a.bias) {
-                f0 = __fadd_rn(f0, bias_s[c + 8 * j + 2 * e]);
-                f1 = __fadd_rn(f1, bias_s[c + 8 * j + 2 * e + 1]);
+                f0 = __fadd_rn(f0, bias_s[c + k]);
+                f1 = __fadd_rn(f1, bias_s[c + k + 1]);
               }
-              const __half h0 = __float2half_rn(__fadd_rn(0.f, f0));
-              const __half h1 = __float2half_rn(__fadd_rn(0.f, f1));
-              uint32_t u = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-              if (!mv) u = 0;
-              bad |= ((u & 0x7c00u) == 0x7c00u) | ((u & 0x7c000000u) == 0x7c000000u);
-              pk[e] = u;
+              const __half2 h = __floats2half2_rn(__fadd_rn(0.f, f0), __fadd_rn(0.f, f1));
+              pk[e] = mv ? *reinterpret_cast<const uint32_t*>(&h) : 0u;
+            }
+            if (a.nonfinite) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                bad |= ((pk[e] & 0x7c00u) == 0x7c00u) | ((pk[e] & 0x7c000000u) == 0x7c000000u);
             }
             *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
                 make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -478,9 +571,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_lo; c < c_hi; c += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
+        tmem_ld32_nowait(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
+        tmem_wait_ld();
         const int nb = n0 + c;
         const bool full_cols = nb + 32 <= a.N;
         if (a.partial) {
@@ -569,8 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[ab]);
       if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
       if (a.stats) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int col = tid; col < BN; col += 128) {
+        named_sync(1, kEpiThreads);
+        for (int col = tid; col < BN; col += kEpiThreads) {
           if (n0 + col >= a.N) continue;
           float t1 = 0.f, t2 = 0.f;
 #pragma unroll
@@ -582,11 +676,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           stat_s[n0 + col] += t1;
           stat_s[C::MAX_STAT_N + n0 + col] += t2;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        named_sync(1, kEpiThreads);
       }
     }
     if (a.stats) {  // one partial row per CTA: stats[blockIdx.x][2][N]
-      for (int col = tid; col < a.N; col += 128) {
+      for (int col = tid; col < a.N; col += kEpiThreads) {
         a.stats[((int64_t)blockIdx.x * 2 + 0) * a.N + col] = stat_s[col];
         a.stats[((int64_t)blockIdx.x * 2 + 1) * a.N + col] = stat_s[C::MAX_STAT_N + col];
       }
@@ -606,12 +700,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 // writes D[m][n] to out[n*ldc + m]
 __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __restrict__ partial,
                                    const __half* __restrict__ bias, __half* __restrict__ out,
-                                   int64_t ldc, int acc, int trans, int32_t* nonfinite) {
+                                   int64_t ldc, int acc, int trans, int c4, int c4_s2,
+                                   int fr, int fs, int32_t* nonfinite) {
   int bad = 0;
   const int64_t total = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / N, n = i % N;
+    const int64_t m = i / N;
+    int64_t n = i % N;
+    if (c4) {  // column (r, s, 4-channel slot) -> (r, s, channel); padding dropped
+      const int rw = c4_s2 * 4;
+      const int r = (int)(n / rw), sx = (int)(n % rw) >> 2, c = (int)(n & 3);
+      if (c >= c4 || sx >= fs || r >= fr) continue;
+      n = ((int64_t)r * fs + sx) * c4 + c;
+    }
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + i];
     if (bias) s = __fadd_rn(s, __half2float(bias[n]));
@@ -622,6 +724,32 @@ __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __rest
     bad |= !isfinite(__half2float(h));
   }
   if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+}
+
+// x[n][h][w][c] (c <= 4) -> x4[n][h][w4][4]: image column w at w4 = w + off,
+// zero channel and border padding
+__global__ void k_pad_c4(int pix4, int w, int w4, int off, int c, const __half* __restrict__ x,
+                         uint2* __restrict__ x4) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < pix4; i += gridDim.x * blockDim.x) {
+    const int col = i % w4 - off, nh = i / w4;
+    __align__(8) __half v[4] = {__float2half(0.f), __float2half(0.f), __float2half(0.f),
+                                __float2half(0.f)};
+    if ((unsigned)col < (unsigned)w)
+      for (int j = 0; j < c; ++j) v[j] = x[((int64_t)nh * w + col) * c + j];
+    x4[i] = *reinterpret_cast<const uint2*>(v);
+  }
+}
+
+// W[k][r][s][c] -> wp[k][kp] with wp[k][(r*s2 + s)*4 + c], zeros elsewhere
+__global__ void k_pad_w_c4(int k, int fr, int fs, int s2, int c, int kp,
+                           const __half* __restrict__ w, __half* __restrict__ wp) {
+  const int total = k * kp;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int col = i % kp, row = i / kp;
+    const int r = col / (s2 * 4), sx = (col % (s2 * 4)) >> 2, ch = col & 3;
+    wp[i] = (r < fr && sx < fs && ch < c) ? w[(((int64_t)row * fr + r) * fs + sx) * c + ch]
+                                          : __float2half(0.f);
+  }
 }
 
 // explicit im2col for convolutions whose channel count is not a multiple of
@@ -811,6 +939,9 @@ struct Plan {
   int64_t ldc = 0;
   int splits = 1, kb_per_split = 0, num_kb = 0, tiles_m = 0, tiles_n = 0, units = 0;
   size_t ws_im2col = 0, ws_wpad = 0, ws_partial = 0;
+  bool c4 = false;       // narrow-channel path over a 4-channel padded copy of x
+  size_t ws_x4 = 0;
+  int c4_s2 = 0, c4_w4 = 0, c4_off = 0, c4_pair = 0;
 };
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -879,6 +1010,19 @@ static bool strided_ok(const ConvGeom& g) {
   return g.sh * g.sw <= 16;
 }
 
+// narrow-channel layout: filter rows padded to an even tap count; with an even
+// horizontal stride the x4 copy gets a column shift making tap pairs 16 B loads
+static void c4_layout(const ConvGeom& g, Plan& pl) {
+  pl.c4 = true;
+  pl.c4_s2 = g.s + (g.s & 1);
+  pl.c4_pair = g.sw % 2 == 0;
+  pl.c4_off = pl.c4_pair ? (g.pw & 1) : 0;
+  pl.c4_w4 = g.w + pl.c4_off;
+  if (pl.c4_pair) pl.c4_w4 += pl.c4_w4 & 1;
+  pl.kp = (int)cdiv((int64_t)g.r * pl.c4_s2 * 4, 64) * 64;
+  pl.ws_x4 = (size_t)g.n * g.h * pl.c4_w4 * 8;
+}
+
 static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   Plan pl;
   const ConvGeom& g = pb.g;
@@ -921,6 +1065,12 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       } else {
         pl.amode = A_GATHER_FPROP; pl.gsrc = pb.a; pl.cblk = g.c / 64;
       }
+    } else if (g.c <= 4) {
+      c4_layout(g, pl);
+      pl.K = pl.kp;
+      pl.amode = A_GATHER_C4;
+      pl.bmode = B_TMA_K; pl.B = {nullptr, g.k, pl.kp, pl.kp};
+      pl.ws_wpad = (size_t)g.k * pl.kp * 2;
     } else {
       pl.im2col = true;
       pl.kp = (int)cdiv(rsc, 64) * 64;
@@ -977,6 +1127,11 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       } else {
         pl.bmode = B_GATHER_WGRAD; pl.gsrc = pb.b; pl.cblk = g.c / 64;
       }
+    } else if (g.c <= 4) {
+      // columns in (r, s, 4-channel) order; the f32 reduction maps them back
+      c4_layout(g, pl);
+      pl.N = pl.kp;
+      pl.bmode = B_GATHER_C4;
     } else {
       pl.im2col = true;
       pl.kp = (int)cdiv(rsc, 64) * 64;
@@ -1004,7 +1159,8 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   pl.kb_per_split = (int)cdiv(pl.num_kb, splits);
   pl.splits = (int)cdiv(pl.num_kb, pl.kb_per_split);
   pl.units = tiles * pl.splits;
-  if (pl.splits > 1) pl.ws_partial = (size_t)pl.splits * pl.M * pl.N * 4;
+  if (pl.splits > 1 || (pl.c4 && pb.mode == kWgrad))
+    pl.ws_partial = (size_t)pl.splits * pl.M * pl.N * 4;
   pl.ok = pl.M > 0 && pl.N > 0 && pl.K > 0;
   return pl;
 }
@@ -1039,6 +1195,8 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   NNL_TC_CASE(A_IM2COL, B_TMA_K)
   NNL_TC_CASE(A_IM2COL, B_TMA_MN)
   NNL_TC_CASE(A_TMA_MN, B_IM2COL)
+  NNL_TC_CASE(A_GATHER_C4, B_TMA_K)
+  NNL_TC_CASE(A_TMA_MN, B_GATHER_C4)
 #undef NNL_TC_CASE
   return fail(NNL_ERR_UNSUPPORTED, "no tcgen05 kernel for mode %d/%d", pl.amode, pl.bmode);
 }
@@ -1051,13 +1209,13 @@ bool tc_eligible(const GemmProblem& pb, int dtype) {
 size_t tc_ws_bytes(const GemmProblem& pb) {
   Plan pl = make_plan(pb);
   if (!pl.ok) return 0;
-  size_t w = pl.ws_im2col + pl.ws_wpad + pl.ws_partial;
+  size_t w = pl.ws_im2col + pl.ws_wpad + pl.ws_partial + pl.ws_x4;
   for (int cls = 1; cls < pl.nclass; ++cls) {
     Plan q = make_plan(pb, cls);
-    const size_t v = q.ws_im2col + q.ws_wpad + q.ws_partial;
+    const size_t v = q.ws_im2col + q.ws_wpad + q.ws_partial + q.ws_x4;
     if (v > w) w = v;
   }
-  return w + 3 * 256;
+  return w + 4 * 256;
 }
 
 int32_t tc_stat_rows(const GemmProblem& pb, int dtype) {
@@ -1096,6 +1254,8 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   __half* col = nullptr;
   __half* wpad = nullptr;
   float* partial = nullptr;
+  __half* x4 = nullptr;
+  if (pl.ws_x4) { x4 = reinterpret_cast<__half*>(w); w = align256(w + pl.ws_x4); }
   if (pl.ws_im2col) { col = reinterpret_cast<__half*>(w); w = align256(w + pl.ws_im2col); }
   if (pl.ws_wpad) { wpad = reinterpret_cast<__half*>(w); w = align256(w + pl.ws_wpad); }
   if (pl.ws_partial) partial = reinterpret_cast<float*>(w);
@@ -1107,6 +1267,22 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
                                                                           src, col);
     NNL_CHECK_LAUNCH();
     if (pb.mode == kFprop) pl.A.ptr = col; else pl.B.ptr = col;
+  }
+  if (pl.c4) {
+    const __half* src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
+    const int64_t pix = (int64_t)g.n * g.h * pl.c4_w4;
+    if (pix >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "narrow-channel input too large");
+    k_pad_c4<<<grid_for(pix, 256, 148 * 16), 256, 0, st>>>(
+        (int)pix, g.w, pl.c4_w4, pl.c4_off, g.c, src, reinterpret_cast<uint2*>(x4));
+    NNL_CHECK_LAUNCH();
+    pl.gsrc = x4;
+    if (pb.mode == kFprop) {
+      const int total = g.k * pl.kp;
+      k_pad_w_c4<<<grid_for(total, 256), 256, 0, st>>>(g.k, g.r, g.s, pl.c4_s2, g.c, pl.kp,
+                                                        reinterpret_cast<const __half*>(pb.b), wpad);
+      NNL_CHECK_LAUNCH();
+      pl.B.ptr = wpad;
+    }
   }
   if (pl.pad_w) {
     const int total = g.k * pl.kp;
@@ -1157,8 +1333,11 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   memcpy(args.tap_offh, pl.tap_offh, sizeof(args.tap_offh));
   args.bias = reinterpret_cast<const __half*>(pb.bias);
   args.stats = pb.stats; args.nonfinite = pb.nonfinite;
-  args.partial = pl.splits > 1 ? partial : nullptr;
-  if (pl.splits > 1) {  // bias / accumulate / rounding happen in the reduction
+  args.K = pl.K;
+  args.c4_s2 = pl.c4_s2; args.c4_w4 = pl.c4_w4; args.c4_off = pl.c4_off; args.c4_pair = pl.c4_pair;
+  const bool to_partial = pl.splits > 1 || (pl.c4 && pb.mode == kWgrad);
+  args.partial = to_partial ? partial : nullptr;
+  if (to_partial) {  // bias / accumulate / rounding happen in the reduction
     args.bias = nullptr; args.acc = 0; args.nonfinite = nullptr; args.stats = nullptr;
     if (pl.remap) return fail(NNL_ERR_UNSUPPORTED, "split-K with row remap");
   }
@@ -1175,10 +1354,12 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   else if (pl.bn == 128) rc = dispatch_bn<128>(pl, ta, tb, tc, args, st);
   else rc = dispatch_bn<256>(pl, ta, tb, tc, args, st);
   if (rc) return rc;
-  if (pl.splits > 1) {
+  if (to_partial) {
+    const int c4 = pl.c4 && pb.mode == kWgrad ? g.c : 0;
     k_tc_splitk_reduce<<<grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st>>>(
         pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
-        reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, pb.nonfinite);
+        reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, c4, pl.c4_s2, g.r, g.s,
+        pb.nonfinite);
     NNL_CHECK_LAUNCH();
   }
   return NNL_OK;

@@ -399,7 +399,7 @@ class BatchNormalization(FunctionImpl):
     def can_fuse_relu(self, node) -> bool:
         return True
 
-    def _forward(self, node, y: NdArray, relu: bool):
+    def _forward(self, node, y: NdArray, relu: bool, residual: NdArray | None = None):
         x, gamma, beta, mean, var = (v.data for v in node.inputs)
         c = x.shape[1]
         rows = self._rows(x)
@@ -413,12 +413,13 @@ class BatchNormalization(FunctionImpl):
             ws = _lib.workspace(_lib.lib().nnl_bn_workspace_size(rows, c))
             _lib.call("nnl_bn_fwd_train", x.code, rows, c, x.ptr, gamma.ptr, beta.ptr, mean.ptr,
                       var.ptr, float(np.float32(self.eps)), float(np.float32(self.momentum)),
-                      parts, nparts, sm.data_ptr(), si.data_ptr(), y.ptr, 1 if relu else 0,
+                      parts, nparts, sm.data_ptr(), si.data_ptr(), y.ptr,
+                      residual.ptr if residual is not None else None, 1 if relu else 0,
                       ws[0], ws[1], _st())
         else:
             _lib.call("nnl_bn_fwd_eval", x.code, rows, c, x.ptr, gamma.ptr, beta.ptr, mean.ptr,
                       var.ptr, float(np.float32(self.eps)), sm.data_ptr(), si.data_ptr(), y.ptr,
-                      1 if relu else 0, _st())
+                      residual.ptr if residual is not None else None, 1 if relu else 0, _st())
 
     def forward(self, node, xs, ys):
         self._forward(node, ys[0], relu=False)
@@ -427,7 +428,8 @@ class BatchNormalization(FunctionImpl):
         # backward recomputes the ReLU gate from x, so the output may be released
         self._forward(node, relu_node.outputs[0].data, relu=True)
 
-    def _backward(self, node, gy: NdArray, fused_relu: bool, gxs, acc):
+    def _backward(self, node, gy: NdArray, fused_relu: bool, gxs, acc, gate=None, dres=None,
+                  acc_res=False):
         x = node.inputs[0].data
         gamma = node.inputs[1].data
         beta = node.inputs[2].data
@@ -439,6 +441,8 @@ class BatchNormalization(FunctionImpl):
         if gxs[0] is not None and conv is not None and conv.state.get("bias_by_bn"):
             cbias = conv.inputs[2].grad.ptr  # sole consumer: first contribution overwrites
         _lib.call("nnl_bn_bwd", x.code, rows, c, x.ptr, gy.ptr, 1 if fused_relu else 0,
+                  gate.ptr if gate is not None else None,
+                  dres.ptr if dres is not None else None, _flag(acc_res),
                   gamma.ptr, beta.ptr,
                   node.state["mean"].data_ptr(), node.state["istd"].data_ptr(),
                   1 if self.batch_stat else 0,
@@ -452,6 +456,16 @@ class BatchNormalization(FunctionImpl):
 
     def backward_fused(self, node, relu_node, gxs, acc):
         self._backward(node, relu_node.outputs[0].grad, True, gxs, acc)
+
+    # residual tail BN -> Add2 -> ReLU (engine fusion, graph.py::_plan): the
+    # BN output and the Add2 output are never materialised
+    def forward_residual(self, node, residual: NdArray, relu_node):
+        relu_node.state["keep_output"] = True  # the backward gate
+        self._forward(node, relu_node.outputs[0].data, relu=True, residual=residual)
+
+    def backward_residual(self, node, relu_node, gxs, acc, dres, acc_res):
+        z = relu_node.outputs[0]
+        self._backward(node, z.grad, False, gxs, acc, gate=z.data, dres=dres, acc_res=acc_res)
 
     def backward_reads_input(self, index):
         return index in (0, 1)

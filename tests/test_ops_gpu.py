@@ -205,3 +205,70 @@ def test_bn_train_streaming_vs_oracle(nnl, shape, relu):
     close(xv.g, ox.grad, 1e-2, 2e-3)
     close(ps[2].d, om.value, 1e-5, 1e-5)      # running mean (f32)
     close(ps[3].d, ov.value, 1e-4, 1e-5)      # running var (f32, biased batch var)
+
+
+def _residual_graph(nn, F, x, s, gam, bet, w, lab, shared):
+    """relu(add2(BN(x), s)) [-> add2(., s) when `shared`] -> GAP -> affine -> SCE."""
+    c = x.shape[1]
+    xv = nn.Variable(x.shape, need_grad=True)
+    sv = nn.Variable(s.shape, need_grad=True)
+    xv.d, sv.d = x, s
+    ps = []
+    for a, ng in ((gam, True), (bet, True), (np.zeros(c, np.float32), False),
+                  (np.ones(c, np.float32), False)):
+        v = nn.Variable((c,), need_grad=ng, dtype=nn.Dtype.F32)
+        v.d = a
+        ps.append(v)
+    z = F.relu(F.add2(F.batch_normalization(xv, *ps), sv))
+    if shared:  # a later consumer of s: the tail's shortcut gradient accumulates
+        z = F.add2(z, sv)
+    wv = nn.Variable(w.shape, need_grad=True)
+    bv = nn.Variable((w.shape[1],), need_grad=True)
+    wv.d, bv.d = w, np.zeros(w.shape[1], np.float32)
+    tv = nn.Variable(lab.shape)
+    tv.d = lab
+    loss = F.softmax_cross_entropy(F.affine(F.global_average_pooling(z), wv, bv), tv)
+    return loss, xv, sv, ps
+
+
+@pytest.mark.parametrize("half,c", [(True, 64), (True, 12), (False, 16)])
+@pytest.mark.parametrize("shared", [False, True])
+def test_bn_residual_tail(nnl, half, c, shared):
+    """The engine's residual-tail fusion (BN -> Add2 -> ReLU in one forward
+    pass and one gated backward that also writes the shortcut gradient) is
+    bit-identical to the unfused chain and matches the oracle."""
+    import paper_2102_06725_b200.functions as F
+    _ctx(nnl, half)
+    rng = np.random.default_rng(c + shared)
+    shape = (4, c, 6, 6)
+    x = rng.uniform(-2, 3, shape).astype(np.float32)
+    s = rng.uniform(-1, 1, shape).astype(np.float32)
+    gam = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    bet = rng.uniform(-0.5, 0.5, c).astype(np.float32)
+    w = rng.uniform(-0.5, 0.5, (c, 5)).astype(np.float32)
+    lab = (np.arange(4) % 5).astype(np.float32)
+    runs = []
+    for clear in (True, False):
+        loss, xv, sv, ps = _residual_graph(nnl, F, x, s, gam, bet, w, lab, shared)
+        loss.forward(clear_buffer=clear)
+        loss.backward(8.0, clear_buffer=clear)
+        runs.append([float(loss.d), xv.g.copy(), sv.g.copy(), ps[0].g.copy(), ps[1].g.copy(),
+                     ps[2].d.copy(), ps[3].d.copy()])
+    for a, b in zip(*runs):
+        assert np.array_equal(np.asarray(a), np.asarray(b), equal_nan=True)
+    # oracle
+    ox, os_ = O.Var(x, half=half, need_grad=True), O.Var(s, half=half, need_grad=True)
+    og, ob = O.Var(gam, need_grad=True), O.Var(bet, need_grad=True)
+    om, ov = O.Var(np.zeros(c, np.float32)), O.Var(np.ones(c, np.float32))
+    oz = O.relu(O.add2(O.batch_norm(ox, og, ob, om, ov, half), os_, half), half)
+    if shared:
+        oz = O.add2(oz, os_, half)
+    ow, obias = O.Var(w, half=half, need_grad=True), O.Var(np.zeros(5, np.float32), half=half)
+    ol = O.softmax_ce(O.affine(O.gap(oz, half), ow, obias, half), O.Var(lab), half)
+    O.backward(ol, 8.0)
+    tol = (2e-2, 2e-3) if half else (1e-4, 1e-6)
+    close(runs[0][0], ol.value, *tol)
+    for got, want in ((runs[0][1], ox.grad), (runs[0][2], os_.grad), (runs[0][3], og.grad),
+                      (runs[0][4], ob.grad)):
+        scale = np.abs(want).max() + 1e-6
+        assert np.abs(np.asarray(got, np.float64) - want).max() / scale < (2e-2 if half else 1e-4)

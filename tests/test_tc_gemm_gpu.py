@@ -15,7 +15,14 @@ CONV = [  # (B, cin, cout, k, stride, pad, hw)
     (2, 64, 64, 3, 1, 1, 8),       # 3x3 gather, BN=64
     (3, 128, 128, 3, 2, 1, 9),     # strided 3x3, ragged M tail
     (2, 64, 256, 1, 2, 0, 10),     # 1x1 s2 (downsample)
-    (2, 3, 64, 7, 2, 3, 20),       # stem: explicit im2col
+    (2, 3, 64, 7, 2, 3, 20),       # stem: 4-channel padded gather (A / B)
+    (8, 3, 64, 7, 2, 3, 64),       # stem: many k-blocks, split-K wgrad
+    (3, 1, 16, 5, 1, 0, 12),       # 1 channel (LeNet conv1), ragged taps
+    (2, 3, 32, 5, 2, 2, 17),       # stride 2, even pad, odd width: pair loads, no shift
+    (2, 2, 16, 3, 2, 0, 15),       # stride 2, pad 0, 2 channels
+    (2, 3, 24, 4, 2, 1, 12),       # even filter width (no padded tap slot)
+    (2, 4, 64, 3, 1, 1, 10),       # 4 channels: no channel padding
+    (2, 12, 64, 3, 1, 1, 10),      # 12 channels: explicit im2col
     (4, 256, 64, 1, 1, 0, 7),      # 1x1 reduce, 7x7 maps
     (8, 256, 512, 1, 1, 0, 14),    # 256-wide tiles
     (4, 256, 512, 1, 2, 0, 14),    # 1x1 s2 dgrad: row remap + zero fill
@@ -31,7 +38,7 @@ def test_conv_backward_accumulate_mode(nnl):
     import paper_2102_06725_b200.functions as F
     _half(nnl)
     for geom in [(2, 64, 128, 1, 2, 0, 8), (2, 64, 64, 3, 1, 1, 8), (2, 128, 256, 1, 1, 0, 6),
-                 (2, 64, 64, 3, 2, 1, 10)]:
+                 (2, 64, 64, 3, 2, 1, 10), (2, 3, 64, 7, 2, 3, 20)]:
         b, cin, cout, k, s, p, hw = geom
         rng = np.random.default_rng(k + cout)
         x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
@@ -123,29 +130,34 @@ def test_conv_tc_matches_simt_kernel(nnl):
         assert _rel_err(a, b) < 2e-3
 
 
-def test_conv_stats_epilogue(nnl):
+@pytest.mark.parametrize("geom", [(3, 64, 64, 3, 1, 1, 9), (2, 3, 64, 7, 2, 3, 30),
+                                  (4, 64, 40, 1, 1, 0, 12), (2, 64, 256, 1, 1, 0, 20)])
+def test_conv_stats_epilogue(nnl, geom):
     """BN partial statistics from the conv epilogue equal column sums of the
-    rounded output."""
+    rounded output (3x3 gather, narrow-channel stem, ragged N, 256-wide tiles)."""
     import paper_2102_06725_b200.functions as F
-    from paper_2102_06725_b200 import _lib
     _half(nnl)
+    b, cin, cout, k, s, p, hw = geom
     rng = np.random.default_rng(1)
-    x = rng.uniform(-1, 1, (3, 64, 9, 9)).astype(np.float32)
-    w = rng.uniform(-0.1, 0.1, (64, 64, 3, 3)).astype(np.float32)
-    vs = [nnl.Variable(a.shape) for a in (x, w, np.zeros(64, np.float32))]
-    for v, a in zip(vs, (x, w, np.zeros(64, np.float32))):
+    x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (cout, cin, k, k)).astype(np.float32)
+    vs = [nnl.Variable(a.shape) for a in (x, w, np.zeros(cout, np.float32))]
+    for v, a in zip(vs, (x, w, np.zeros(cout, np.float32))):
         v.d = a
-    y = F.convolution(*vs, stride=(1, 1), pad=(1, 1))
+    y = F.convolution(*vs, stride=(s, s), pad=(p, p))
     node = y.parent
     node.state["emit_stats"] = True
     node.impl.forward(node, [v.data for v in vs], [y.data])
     y.data.mark_set()
     st = y.parent.state["stats"].cpu().numpy()
     rows = y.parent.state["stat_rows"]
-    parts = st[: rows * 2 * 64].reshape(rows, 2, 64)
-    yd = y.d.transpose(0, 2, 3, 1).reshape(-1, 64).astype(np.float64)
+    assert rows > 0
+    parts = st[: rows * 2 * cout].reshape(rows, 2, cout)
+    yd = y.d.transpose(0, 2, 3, 1).reshape(-1, cout).astype(np.float64)
     np.testing.assert_allclose(parts[:, 0].sum(0), yd.sum(0), rtol=1e-4, atol=1e-3)
     np.testing.assert_allclose(parts[:, 1].sum(0), (yd ** 2).sum(0), rtol=1e-4, atol=1e-3)
+    ov = [O.Var(a, half=True) for a in (x, w, np.zeros(cout, np.float32))]
+    assert _rel_err(y.d, O.conv2d(*ov, (s, s), (p, p), True).value) < 4e-3
 
 
 @pytest.mark.parametrize("dims", [(32, 128, 64), (16, 256, 1000), (256, 2048, 1000)])

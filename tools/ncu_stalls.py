@@ -6,9 +6,18 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
-data = rows[2:]
+def _num(x):
+    try:
+        float(x or 0)
+        return True
+    except ValueError:
+        return False
+
+
+data = [r for r in rows[2:] if len(r) == len(hdr)]
 i_s = hdr.index("Warp Stall Sampling (All Samples)")
 i_src = hdr.index("Source")
+data = [r for r in data if _num(r[i_s])]
 reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 tot = sum(float(r[i_s] or 0) for r in data if "EXIT" not in r[i_src])
 mix = {h: sum(float(r[hdr.index(h)] or 0) for r in data if "EXIT" not in r[i_src]) for h in reasons}
