@@ -946,17 +946,20 @@ struct Plan {
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// tile width with the smallest (waves x width) cost; ties go to the wider tile
+// tile width with the smallest (waves x per-tile time) cost.  A 128 x BN
+// tile's k-step moves (128 + BN) x 64 operand elements through L2 -> SMEM,
+// which bounds the mainloop (85 FLOP/B at BN = 256, 64 at 128: measured
+// ~13 TB/s aggregate), so per-tile time ~ (128 + BN); ties go to the wider tile
 static int pick_bn(const Plan& pl, bool tap_split_b) {
   if (pl.N <= 64) return 64;
   const int sms = num_sms();
   int best = 128;
   double best_cost = 1e30;
-  for (int bn : {128, 256}) {
+  for (int bn : {256, 128}) {
     if (bn == 256 && pl.N <= 128) continue;
     if (tap_split_b && pl.N % bn) continue;  // dgrad B tiles must not straddle taps
     const int64_t units = cdiv(pl.M, BM) * cdiv(pl.N, bn);
-    const double cost = (double)cdiv(units, sms) * bn * (bn == 128 ? 1.05 : 1.0);
+    const double cost = (double)cdiv(units, sms) * (128 + bn);
     if (cost < best_cost) {
       best_cost = cost;
       best = bn;
@@ -1150,11 +1153,24 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   int splits = 1;
   const int sms = num_sms();
   if (tiles < sms && pb.stats == nullptr && !pl.remap) {
-    splits = (int)cdiv(2 * sms, tiles);
-    const int max_by_k = pl.num_kb / 4;
-    if (splits > max_by_k) splits = max_by_k;
-    if (splits > 128) splits = 128;
-    if (splits < 1) splits = 1;
+    // wave-quantisation-aware choice: cost in k-block times of the busiest
+    // CTA (waves x (k-blocks per unit + epilogue)) plus the f32 partial
+    // round trip of the fixed-order reduction (~0.26 us per k-block at
+    // 128 x 256, partials at ~6 TB/s)
+    int max_s = pl.num_kb / 4 < 4 * sms ? pl.num_kb / 4 : 4 * sms;
+    while (max_s > 1 && (double)max_s * pl.M * pl.N * 4.0 > 256e6) --max_s;
+    double best = 1e30;
+    for (int s = 1; s <= (max_s > 1 ? max_s : 1); ++s) {
+      const int64_t waves = cdiv((int64_t)tiles * s, sms);
+      const int64_t per = cdiv(pl.num_kb, s);
+      if (s > 1 && cdiv(pl.num_kb, per) < s) continue;  // empty splits
+      const double red = s > 1 ? (double)s * pl.M * pl.N * 8.0 / 6e12 / 0.26e-6 : 0.0;
+      const double cost = (double)waves * (per + 2) + red;
+      if (cost < best) {
+        best = cost;
+        splits = s;
+      }
+    }
   }
   pl.kb_per_split = (int)cdiv(pl.num_kb, splits);
   pl.splits = (int)cdiv(pl.num_kb, pl.kb_per_split);
