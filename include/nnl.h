@@ -52,6 +52,10 @@ int nnl_version(void);
 int64_t nnl_launch_count(int reset);
 /* 1 when the tensor-core (tcgen05) path is enabled for eligible shapes */
 int nnl_set_tc_enabled(int enabled);
+/* CTA-pair (tcgen05 cta_group::2) tiles: 0 off, 1 cost heuristic (default),
+   2 whenever eligible; returns the previous setting, < 0 only queries
+   (initial value from env NNL_TC_PAIRS) */
+int nnl_set_tc_pairs(int enabled);
 
 /* ---- geometry ----------------------------------------------------------- */
 typedef struct nnl_conv_shape {

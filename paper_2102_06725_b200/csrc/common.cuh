@@ -16,6 +16,7 @@ void set_error(const std::string& msg);
 int fail(int code, const char* fmt, ...);
 void count_launch(int n = 1);
 extern int g_tc_enabled;
+extern int g_tc_pairs;
 
 #define NNL_CHECK_LAUNCH()                                                      \
   do {                                                                          \

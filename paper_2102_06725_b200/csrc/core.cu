@@ -15,6 +15,8 @@ namespace nnl {
 static thread_local std::string t_last_error;
 static std::atomic<int64_t> g_launches{0};
 int g_tc_enabled = 1;
+// CTA-pair (cta_group::2) tiles for long-K GEMMs; NNL_TC_PAIRS=0 disables
+int g_tc_pairs = -1;
 
 void set_error(const std::string& msg) { t_last_error = msg; }
 
@@ -286,6 +288,15 @@ int64_t nnl_launch_count(int reset) {
 int nnl_set_tc_enabled(int enabled) {
   int prev = g_tc_enabled;
   g_tc_enabled = enabled;
+  return prev;
+}
+int nnl_set_tc_pairs(int enabled) {
+  if (g_tc_pairs < 0) {
+    const char* e = getenv("NNL_TC_PAIRS");
+    g_tc_pairs = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
+  }
+  int prev = g_tc_pairs;
+  if (enabled >= 0) g_tc_pairs = enabled > 2 ? 2 : enabled;
   return prev;
 }
 

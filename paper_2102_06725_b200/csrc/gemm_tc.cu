@@ -42,21 +42,28 @@ enum BMode { B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATH
 
 constexpr int BM = 128, BK = 64, kThreads = 384;
 
-template <int BN>
+// CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2; each CTA holds its 128 rows of A and BN/2 columns
+// of B, so one k-step moves (256 + BN) x 64 operand elements through L2 for
+// 2 x 128 x BN outputs instead of 2 x (128 + BN) x 64.
+template <int BN, int CG = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 5 : 7);
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;  // this CTA's share of B
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int PIPE = STAGES * (A_BYTES + B_BYTES);
   static constexpr int RED_BYTES = 4 * BN * 2 * 4;
   static constexpr int BIAS_BYTES = BN * 4;
   static constexpr int MAX_STAT_N = 2048;  // per-CTA BN statistics accumulator [2][N]
   static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
-  // TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 64 cols fp16)
+  // TMA-store staging: 8 x 4 KB (4 warps x 2 buffers, or 8 warps x 1)
   static constexpr int STG_BYTES = 4 * 2 * 4096;
-  static constexpr int SMEM =
-      PIPE + 1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + STG_BYTES + 1024;
+  static constexpr int FIXED = 1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + STG_BYTES + 1024;
+  static constexpr int BUDGET = 232448;
+  static constexpr int STAGES_FIT = (BUDGET - FIXED) / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int PIPE = STAGES * (A_BYTES + B_BYTES);
+  static constexpr int SMEM = PIPE + FIXED;
+  static_assert(STAGES >= 3, "pipeline too shallow");
 };
 
 struct TcArgs {
@@ -132,18 +139,20 @@ __device__ __forceinline__ void c4_chunk(uint8_t* dst, const TcArgs& a, const Co
   }
 }
 
-template <int BN, int AM, int BMD>
+template <int BN, int AM, int BMD, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const TcArgs a) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   constexpr int S = C::STAGES;
+  constexpr int BNL = BN / CG;  // B columns held by this CTA
   constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD || AM == A_GATHER_C4;
   constexpr bool kGB = BMD == B_GATHER_WGRAD || BMD == B_GATHER_C4;
   constexpr bool kAmn = AM == A_TMA_MN;
   constexpr bool kBmn = BMD != B_TMA_K;
   constexpr uint32_t kTmaBytes = (kGA ? 0 : C::A_BYTES) + (kGB ? 0 : C::B_BYTES);
-  constexpr uint32_t IDESC = idesc_f16(BN, kAmn, kBmn);
+  constexpr uint32_t IDESC = idesc_f16(BN, kAmn, kBmn, 128 * CG);
+  static_assert(CG == 1 || (!kGA && !kGB), "CTA pairs need TMA-fed operands");
   // TMA-fed tiles leave warps 4..7 free: they join the epilogue
   constexpr bool kEpi8 = !kGA && !kGB && BN >= 128;
   constexpr int kEpi = kEpi8 ? 8 : 4, kEpiWarp0 = kEpi8 ? 4 : 8;
@@ -169,6 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ConvGeom& g = a.g;
+  // CTA pair: rank 0 (the leader) owns the full/tempty barriers and issues the
+  // MMAs; units are walked per pair
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -177,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpi);
+      mbar_init(&tempty[b], kEpi * CG);
     }
     fence_barrier_init();
   }
@@ -186,9 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!kGB) tma_prefetch(&tmB);
     if (a.tma_store) tma_prefetch(&tmC);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 2) tmem_alloc_cg<CG>(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -196,9 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (kTmaBytes && lane == 0) {
       int it = 0;
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+      for (int u = pair; u < a.units; u += npairs) {
         const Unit w = decode_unit(a, u);
-        const int m0 = w.tm * BM, n0 = w.tn * BN;
+        // this CTA's A rows and B columns of the (128*CG) x BN tile
+        const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN + rank * BNL;
         // im2col A: window base of the tile's first row pixel
         int a_x = 0, a_y = 0, a_n = 0;
         if (AM == A_IM2COL) {
@@ -212,7 +226,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (it / S) & 1;
           const int kb = w.kb0 + i;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_tx(&full[s], kTmaBytes);
+          // the leader's barrier counts both CTAs' bytes; the peer only loads
+          if (rank == 0) mbar_arrive_tx(&full[s], kTmaBytes * CG);
+          const uint32_t fb = CG == 2 ? mapa_shared(&full[s], 0) : smem_u32(&full[s]);
+          auto load2d = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
+            if (CG == 2) tma_load_2d_cg2(dst, tm, fb, c0, c1);
+            else tma_load_2d(dst, tm, &full[s], c0, c1);
+          };
+          auto loadi2c = [&](void* dst, const CUtensorMap* tm, int c, int w_, int h_, int n_,
+                             uint16_t ow, uint16_t oh) {
+            if (CG == 2) tma_load_im2col_cg2(dst, tm, fb, c, w_, h_, n_, ow, oh);
+            else tma_load_im2col(dst, tm, &full[s], c, w_, h_, n_, ow, oh);
+          };
           if (AM == A_IM2COL) {
             const int t = kb / a.cblk, cb = kb - t * a.cblk;
             int r, sx;
@@ -223,39 +248,38 @@ __global__ void __launch_bounds__(kThreads, 1)
               r = t / g.s;
               sx = t - r * g.s;
             }
-            tma_load_im2col(stA + s * C::A_BYTES, &tmA, &full[s], cb * 64, a_x * a.isw + a.ilw,
-                            a_y * a.ish + a.ilh, a_n, (uint16_t)sx, (uint16_t)r);
+            loadi2c(stA + s * C::A_BYTES, &tmA, cb * 64, a_x * a.isw + a.ilw,
+                    a_y * a.ish + a.ilh, a_n, (uint16_t)sx, (uint16_t)r);
           } else if (AM == A_TMA_K) {
-            tma_load_2d(stA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+            load2d(stA + s * C::A_BYTES, &tmA, kb * BK, m0);
           } else if (AM == A_TMA_MN) {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(stA + s * C::A_BYTES + j * 8192, &tmA, &full[s], m0 + 64 * j, kb * BK);
+              load2d(stA + s * C::A_BYTES + j * 8192, &tmA, m0 + 64 * j, kb * BK);
           }
           if (BMD == B_TMA_K) {
-            tma_load_2d(stB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+            load2d(stB + s * C::B_BYTES, &tmB, kb * BK, n0);
           } else if (BMD == B_TMA_MN) {
             int t = kb / a.b_kblk;
             const int kob = kb - t * a.b_kblk;
             if (a.ntap) t = a.tap_w[t];
             else if (a.flip) t = g.r * g.s - 1 - t;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(stB + s * C::B_BYTES + j * 8192, &tmB, &full[s],
-                          t * a.b_tap_stride + n0 + 64 * j, kob * BK);
+            for (int j = 0; j < BNL / 64; ++j)
+              load2d(stB + s * C::B_BYTES + j * 8192, &tmB, t * a.b_tap_stride + n0 + 64 * j,
+                     kob * BK);
           } else if (BMD == B_IM2COL) {
             // 64 reduction pixels x 64 channels of tap (r, s) per 64-wide N block
             const int pix0 = kb * BK;
             const int bx = pix0 % a.gw, t0 = pix0 / a.gw;
             const int by = t0 % a.gh, bn_ = t0 / a.gh;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
+            for (int j = 0; j < BNL / 64; ++j) {
               const int cbg = (n0 >> 6) + j;
               const int t = cbg / a.cblk, cb = cbg - t * a.cblk;
               const int r = t / g.s, sx = t - r * g.s;
-              tma_load_im2col(stB + s * C::B_BYTES + j * 8192, &tmB, &full[s], cb * 64,
-                              bx * a.isw + a.ilw, by * a.ish + a.ilh, bn_, (uint16_t)sx,
-                              (uint16_t)r);
+              loadi2c(stB + s * C::B_BYTES + j * 8192, &tmB, cb * 64, bx * a.isw + a.ilw,
+                      by * a.ish + a.ilh, bn_, (uint16_t)sx, (uint16_t)r);
             }
           }
         }
@@ -263,9 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       int it = 0, t = 0;
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++t) {
+      for (int u = pair; u < a.units; u += npairs, ++t) {
         const Unit w = decode_unit(a, u);
         const int ab = t & 1;
         mbar_wait(&tempty[ab], ((t >> 1) & 1) ^ 1);
@@ -284,11 +308,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : sdesc_sw128(abase + kk * 32, 16, 1024);
             const uint64_t db = kBmn ? sdesc_sw128(bbase + kk * 2048, 8192, 1024)
                                      : sdesc_sw128(bbase + kk * 32, 16, 1024);
-            mma_f16(d, da, db, IDESC, (i | kk) != 0);
+            if (CG == 2) mma_f16_cg2(d, da, db, IDESC, (i | kk) != 0);
+            else mma_f16(d, da, db, IDESC, (i | kk) != 0);
           }
-          mma_commit(&empty[s]);
+          if (CG == 2) mma_commit_cg2(&empty[s]);
+          else mma_commit(&empty[s]);
         }
-        mma_commit(&tfull[ab]);
+        if (CG == 2) mma_commit_cg2(&tfull[ab]);
+        else mma_commit(&tfull[ab]);
       }
     }
   } else if (!kEpi8 && warp >= 4 && warp < 8) {
@@ -298,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tid = threadIdx.x - 128;
       const int chunk = tid & 7;
       int it = 0;
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+      for (int u = pair; u < a.units; u += npairs) {
         const Unit w = decode_unit(a, u);
         const int m0 = w.tm * BM, n0 = w.tn * BN;
         // per-row metadata of this tile's 8 A rows (fixed across its k-blocks)
@@ -488,9 +515,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     int t = 0;
     uint32_t sb = 0;  // TMA-store staging buffer alternation (per warp)
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++t) {
+    // the leader's tempty barriers (the MMA waits on both CTAs' epilogues)
+    const uint32_t te0 = CG == 2 ? mapa_shared(&tempty[0], 0) : smem_u32(&tempty[0]);
+    for (int u = pair; u < a.units; u += npairs, ++t) {
       const Unit w = decode_unit(a, u);
-      const int m0 = w.tm * BM, n0 = w.tn * BN;
+      const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN;
       const int ab = t & 1;
       if (a.bias) {  // this tile's bias slice, staged once in shared memory (as f32)
         named_sync(2, kEpiThreads);
@@ -660,7 +689,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the accumulator buffer can be reused by the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[ab]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(te0 + 8 * ab);
+        else mbar_arrive(&tempty[ab]);
+      }
       if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
       if (a.stats) {
         named_sync(1, kEpiThreads);
@@ -689,10 +721,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, C::TMEM_COLS);
+    tmem_dealloc_cg<CG>(tmem, C::TMEM_COLS);
   }
 }
 
@@ -894,6 +926,9 @@ static bool use_tma_im2col() {
   return v == 1;
 }
 
+// 0: never, 1: cost heuristic, 2: whenever eligible (tuning)
+static int cta_pair_policy() { return nnl_set_tc_pairs(-1); }
+
 static bool use_tma_store() {
   static int v = -1;
   if (v < 0) {
@@ -939,6 +974,7 @@ struct Plan {
   int64_t ldc = 0;
   int splits = 1, kb_per_split = 0, num_kb = 0, tiles_m = 0, tiles_n = 0, units = 0;
   size_t ws_im2col = 0, ws_wpad = 0, ws_partial = 0;
+  int cg = 1;            // 2: CTA-pair (cta_group::2) 256-row tiles
   bool c4 = false;       // narrow-channel path over a 4-channel padded copy of x
   size_t ws_x4 = 0;
   int c4_s2 = 0, c4_w4 = 0, c4_off = 0, c4_pair = 0;
@@ -1146,62 +1182,99 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   pl.bn = pick_bn(pl, pl.bmode == B_TMA_MN && pl.b_tap_stride && !k1);
   if (pl.remap && pl.N % pl.bn) pl.bn = 64;
   pl.num_kb = (int)cdiv(pl.K, BK);
-  pl.tiles_m = (int)cdiv(pl.M, BM);
-  pl.tiles_n = (int)cdiv(pl.N, pl.bn);
-  const int tiles = pl.tiles_m * pl.tiles_n;
-  // split the reduction when the tile grid cannot fill the machine
-  int splits = 1;
-  const int sms = num_sms();
-  if (tiles < sms && pb.stats == nullptr && !pl.remap) {
-    // wave-quantisation-aware choice: cost in k-block times of the busiest
-    // CTA (waves x (k-blocks per unit + epilogue)) plus the f32 partial
-    // round trip of the fixed-order reduction (~0.26 us per k-block at
-    // 128 x 256, partials at ~6 TB/s)
-    int max_s = pl.num_kb / 4 < 4 * sms ? pl.num_kb / 4 : 4 * sms;
-    while (max_s > 1 && (double)max_s * pl.M * pl.N * 4.0 > 256e6) --max_s;
-    double best = 1e30;
-    for (int s = 1; s <= (max_s > 1 ? max_s : 1); ++s) {
-      const int64_t waves = cdiv((int64_t)tiles * s, sms);
-      const int64_t per = cdiv(pl.num_kb, s);
-      if (s > 1 && cdiv(pl.num_kb, per) < s) continue;  // empty splits
-      const double red = s > 1 ? (double)s * pl.M * pl.N * 8.0 / 6e12 / 0.26e-6 : 0.0;
-      const double cost = (double)waves * (per + 2) + red;
-      if (cost < best) {
-        best = cost;
-        splits = s;
+  auto tile_and_split = [&](int cg) {
+    pl.cg = cg;
+    pl.tiles_m = (int)cdiv(pl.M, BM * cg);
+    pl.tiles_n = (int)cdiv(pl.N, pl.bn);
+    const int tiles = pl.tiles_m * pl.tiles_n;
+    // split the reduction when the tile grid cannot fill the machine
+    int splits = 1;
+    const int sms = num_sms() / cg;  // concurrent work slots (CTAs or CTA pairs)
+    if (tiles < sms && pb.stats == nullptr && !pl.remap) {
+      // wave-quantisation-aware choice: cost in k-block times of the busiest
+      // slot (waves x (k-blocks per unit + epilogue)) plus the f32 partial
+      // round trip of the fixed-order reduction (~0.26 us per k-block at
+      // 128 x 256, partials at ~6 TB/s)
+      int max_s = pl.num_kb / 4 < 4 * sms ? pl.num_kb / 4 : 4 * sms;
+      while (max_s > 1 && (double)max_s * pl.M * pl.N * 4.0 > 256e6) --max_s;
+      double best = 1e30;
+      for (int s = 1; s <= (max_s > 1 ? max_s : 1); ++s) {
+        const int64_t waves = cdiv((int64_t)tiles * s, sms);
+        const int64_t per = cdiv(pl.num_kb, s);
+        if (s > 1 && cdiv(pl.num_kb, per) < s) continue;  // empty splits
+        const double red = s > 1 ? (double)s * pl.M * pl.N * 8.0 / 6e12 / 0.26e-6 : 0.0;
+        const double cost = (double)waves * (per + 2) + red;
+        if (cost < best) {
+          best = cost;
+          splits = s;
+        }
       }
     }
+    pl.kb_per_split = (int)cdiv(pl.num_kb, splits);
+    pl.splits = (int)cdiv(pl.num_kb, pl.kb_per_split);
+    pl.units = tiles * pl.splits;
+  };
+  tile_and_split(1);
+  {
+    // CTA pairs (256-row tiles, half the L2 operand traffic per output) pay off
+    // once the k-loop is long enough for the mainloop, not the per-tile
+    // epilogue, to bound the tile: 256-wide tiles with >= 16 k-blocks per unit
+    const bool a_tma = pl.amode == A_TMA_K || pl.amode == A_TMA_MN || pl.amode == A_IM2COL;
+    const bool b_tma = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN || pl.bmode == B_IM2COL;
+    const int pol = cta_pair_policy();
+    if (pol && a_tma && b_tma && pl.bn >= 128 && pl.M > BM &&
+        (pol == 2 || (pl.bn == 256 && pl.kb_per_split >= 16)))
+      tile_and_split(2);
   }
-  pl.kb_per_split = (int)cdiv(pl.num_kb, splits);
-  pl.splits = (int)cdiv(pl.num_kb, pl.kb_per_split);
-  pl.units = tiles * pl.splits;
   if (pl.splits > 1 || (pl.c4 && pb.mode == kWgrad))
     pl.ws_partial = (size_t)pl.splits * pl.M * pl.N * 4;
   pl.ok = pl.M > 0 && pl.N > 0 && pl.K > 0;
   return pl;
 }
 
-template <int BN, int AM, int BMD>
+static int plan_grid(const Plan& pl) {
+  const int pairs = num_sms() / pl.cg;
+  return (pl.units < pairs ? pl.units : pairs) * pl.cg;
+}
+
+template <int BN, int AM, int BMD, int CG>
 static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
                      const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
-  auto kern = k_tc_gemm<BN, AM, BMD>;
+  auto kern = k_tc_gemm<BN, AM, BMD, CG>;
   static bool attr = false;
   if (!attr) {
     NNL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg<BN>::SMEM));
+                                  Cfg<BN, CG>::SMEM));
     attr = true;
   }
-  const int grid = pl.units < num_sms() ? pl.units : num_sms();
-  kern<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(ta, tb, tc, args);
-  NNL_CHECK_LAUNCH();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)plan_grid(pl));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<BN, CG>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  if (CG == 2) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  NNL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, args));
+  count_launch();
   return NNL_OK;
 }
 
 template <int BN>
 static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
                        const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
-#define NNL_TC_CASE(AM, BMD) \
-  if (pl.amode == AM && pl.bmode == BMD) return launch_tc<BN, AM, BMD>(pl, ta, tb, tc, args, st);
+#define NNL_TC_CASE(AM, BMD)                                                   \
+  if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1)                         \
+    return launch_tc<BN, AM, BMD, 1>(pl, ta, tb, tc, args, st);
+#define NNL_TC_CASE2(AM, BMD)                                                  \
+  if (pl.amode == AM && pl.bmode == BMD && pl.cg == 2)                         \
+    return launch_tc<BN, AM, BMD, 2>(pl, ta, tb, tc, args, st);
   NNL_TC_CASE(A_TMA_K, B_TMA_K)
   NNL_TC_CASE(A_TMA_K, B_TMA_MN)
   NNL_TC_CASE(A_TMA_MN, B_TMA_MN)
@@ -1213,8 +1286,18 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   NNL_TC_CASE(A_TMA_MN, B_IM2COL)
   NNL_TC_CASE(A_GATHER_C4, B_TMA_K)
   NNL_TC_CASE(A_TMA_MN, B_GATHER_C4)
+  if constexpr (BN >= 128) {
+    NNL_TC_CASE2(A_TMA_K, B_TMA_K)
+    NNL_TC_CASE2(A_TMA_K, B_TMA_MN)
+    NNL_TC_CASE2(A_TMA_MN, B_TMA_MN)
+    NNL_TC_CASE2(A_IM2COL, B_TMA_K)
+    NNL_TC_CASE2(A_IM2COL, B_TMA_MN)
+    NNL_TC_CASE2(A_TMA_MN, B_IM2COL)
+  }
 #undef NNL_TC_CASE
-  return fail(NNL_ERR_UNSUPPORTED, "no tcgen05 kernel for mode %d/%d", pl.amode, pl.bmode);
+#undef NNL_TC_CASE2
+  return fail(NNL_ERR_UNSUPPORTED, "no tcgen05 kernel for mode %d/%d cg %d", pl.amode, pl.bmode,
+              pl.cg);
 }
 
 bool tc_eligible(const GemmProblem& pb, int dtype) {
@@ -1242,7 +1325,7 @@ int32_t tc_stat_rows(const GemmProblem& pb, int dtype) {
   Plan pl = make_plan(q);
   if (!pl.ok || pb.mode != kFprop || pb.g.affine || pl.N > Cfg<64>::MAX_STAT_N) return 0;
   // one partial row per persistent CTA
-  return pl.units < num_sms() ? pl.units : num_sms();
+  return plan_grid(pl);
 }
 
 static inline uint8_t* align256(uint8_t* p) {
@@ -1326,7 +1409,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     if ((rc = make_im2col_tmap(&ta, pl.im))) return rc;
   }
   if (pl.bmode == B_TMA_K) {
-    if ((rc = make_tmap(&tb, pl.B, 64, pl.bn))) return rc;
+    if ((rc = make_tmap(&tb, pl.B, 64, pl.bn / pl.cg))) return rc;
   } else if (pl.bmode == B_TMA_MN) {
     if ((rc = make_tmap(&tb, pl.B, 64, 64))) return rc;
   } else if (pl.bmode == B_IM2COL) {

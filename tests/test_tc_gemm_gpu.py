@@ -181,3 +181,32 @@ def test_affine_tc_vs_oracle(nnl, dims):
     assert _rel_err(y.d, oy.value) < 4e-3
     for v, o_ in zip(vs, ov):
         assert _rel_err(v.g, o_.grad) < 4e-3
+
+
+def test_cta_pairs_match_single_cta(nnl):
+    """256-row CTA-pair tiles (tcgen05 cta_group::2) give the same sums as
+    128-row tiles: bit-identical where no split-K is involved (fprop, dgrad),
+    within f32 regrouping of the split-K partials for wgrad."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (128, 256, 14, 14)).astype(np.float32)
+    w = rng.uniform(-0.05, 0.05, (256, 256, 3, 3)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, (256,)).astype(np.float32)
+    outs = []
+    for pairs in (1, 0):
+        prev = _lib.lib().nnl_set_tc_pairs(pairs)
+        try:
+            vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+            for v, a in zip(vs, (x, w, bias)):
+                v.d = a
+            y = F.convolution(*vs, stride=(1, 1), pad=(1, 1))
+            y.forward()
+            y.backward(1.0)
+            outs.append([y.d, vs[0].g, vs[1].g])
+        finally:
+            _lib.lib().nnl_set_tc_pairs(prev)
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert _rel_err(outs[0][2], outs[1][2]) < 2e-3

@@ -55,6 +55,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--cudnn", action="store_true")
     ap.add_argument("--once", action="store_true", help="one call per pass (for ncu)")
+    ap.add_argument("--ab-pairs", action="store_true",
+                    help="also time each pass with CTA pairs disabled (same process)")
     args = ap.parse_args()
     import torch
     from paper_2102_06725_b200 import _lib
@@ -106,22 +108,32 @@ def main():
                 fn()
                 torch.cuda.synchronize()
                 continue
-            for _ in range(args.warmup):
-                fn()
-            times = []
-            for _ in range(args.iters):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                fn()
-                e1.record()
-                torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1))
-            ms = statistics.median(times)
+            def timed():
+                for _ in range(args.warmup):
+                    fn()
+                times = []
+                for _ in range(args.iters):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    fn()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    times.append(e0.elapsed_time(e1))
+                return statistics.median(times)
+
+            ms = timed()
+            extra = ""
+            if args.ab_pairs:
+                prev = L.nnl_set_tc_pairs(0)
+                ms_single = timed()
+                L.nnl_set_tc_pairs(prev)
+                extra += f" single {ms_single:8.3f}"
+                total["single"] = total.get("single", 0.0) + ms_single
             bound_s = max(flops / tpk, byts / hbm)
             tf = flops / (ms / 1e3) / 1e12
             total["ours"] += ms
             total["bound"] += bound_s * 1e3
-            extra = ""
             if args.cudnn:
                 xt = x.permute(0, 3, 1, 2)
                 wt = w.permute(0, 3, 1, 2)
@@ -142,13 +154,14 @@ def main():
                     e1.record()
                     torch.cuda.synchronize()
                     ct.append(e0.elapsed_time(e1))
-                extra = f" {statistics.median(ct):8.3f}"
+                extra += f" cudnn {statistics.median(ct):8.3f}"
             name = f"{b}x{c}x{hw}x{hw}->{k} k{r}s{s}"
             print(f"{name:34s} {ps:6s} {ms:8.3f} {tf:8.1f} {bound_s * 1e3:8.3f} "
                   f"{100 * bound_s * 1e3 / ms:6.1f}{extra}", flush=True)
     if not args.once:
         print(f"TOTAL ours {total['ours']:.3f} ms, per-layer bound {total['bound']:.3f} ms "
-              f"({100 * total['bound'] / max(total['ours'], 1e-9):.1f}% of roofline)")
+              f"({100 * total['bound'] / max(total['ours'], 1e-9):.1f}% of roofline)"
+              + (f"; without CTA pairs {total['single']:.3f} ms" if "single" in total else ""))
 
 
 if __name__ == "__main__":
