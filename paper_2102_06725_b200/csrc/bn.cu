@@ -577,6 +577,7 @@ static int bn_apply_fwd(int dtype, int64_t rows, int32_t c, const void* x, const
     a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)y; a.gamma = gamma;
     a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fuse_relu;
     a.res = (const __half*)residual;
+    a.reverse = 1;
     return bn_stream_launch(BNS_APPLY_F, a, st);
   }
   BnGeom g = bn_geom(c, al16(x) && al16(y));
@@ -671,7 +672,8 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
     a.beta = beta; a.mu = save_mean; a.istd = save_istd; a.relu = fused_relu; a.partials = parts;
     a.gate = (const __half*)gate;
     a.dres = dres_first ? (__half*)dres : nullptr;
-    rc = bn_stream_launch(BNS_STATS_B, a, st);
+    a.reverse = 1;  // dy's producer wrote it first to last; APPLY_B then re-reads
+    rc = bn_stream_launch(BNS_STATS_B, a, st);  // from the start, still in L2
   } else {
     NNL_DISPATCH_DTYPE(dtype, T, {
       rc = launch_partials<T, 1>(rows, c, g, bx, (const T*)x, (const T*)dy, fused_relu,

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
   }
   __syncthreads();
   auto issue = [&](int s, int64_t chunk) {
-    const int64_t r0 = chunk * a.chunk_rows;
+    const int64_t r0 = (a.reverse ? a.nchunks - 1 - chunk : chunk) * a.chunk_rows;
     const int64_t nr = min((int64_t)a.chunk_rows, a.rows - r0);
     const uint32_t bytes = (uint32_t)(nr * a.c * 2);
     mbar_arrive_tx(&full[s], bytes * NT);
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
   for (int64_t ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x, ++it) {
     const int s = it % kStages;
     mbar_wait(&full[s], (it / kStages) & 1);
-    const int64_t r0 = ch * a.chunk_rows;
+    const int64_t r0 = (a.reverse ? a.nchunks - 1 - ch : ch) * a.chunk_rows;
     const int nr = (int)min((int64_t)a.chunk_rows, a.rows - r0);
     const uint8_t* xs = smem + (s * NT + 0) * kChunkBytes;
     const uint8_t* gs = smem + (s * NT + 1) * kChunkBytes;

@@ -28,6 +28,9 @@ struct BnStreamArgs {
   const __half* res;   // APPLY_F: y = relu(q(q(bn(x)) + res)), streamed
   const __half* gate;  // STATS_B / APPLY_B: gy *= (gate > 0), streamed
   __half* dres;        // STATS_B with gate: dres = q(0 + gated gy)
+  // walk the chunks last to first: the tail of a tensor its producer has just
+  // written (or the previous pass has just read) is still in the 126 MB L2
+  int reverse;
 };
 
 bool bn_stream_ok(int64_t rows, int32_t c, const void* a, const void* b, const void* d);
