@@ -35,10 +35,16 @@ using namespace tc;
 // A_GATHER_C4 / B_GATHER_C4: narrow-channel convolutions (the 3-channel stem)
 // over a 4-channel padded copy of x, reduction index k = tap*4 + c, 16 taps per
 // 64-wide k-block, gathered as 8 B pieces.
+// A_IM2COL16 / B_IM2COL16: stride-2 narrow-channel convolutions (the stem)
+// rewritten by space-to-depth as a stride-1 convolution over a 16-channel
+// tensor; TMA im2col with 32-byte rows, one 16-wide K step per filter tap.
 enum AMode {
-  A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4, A_GATHER_C4 = 5
+  A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4,
+  A_GATHER_C4 = 5, A_IM2COL16 = 6
 };
-enum BMode { B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATHER_C4 = 4 };
+enum BMode {
+  B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATHER_C4 = 4, B_IM2COL16 = 5
+};
 
 constexpr int BM = 128, BK = 64, kThreads = 384;
 
@@ -154,9 +160,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t IDESC = idesc_f16(BN, kAmn, kBmn, 128 * CG);
   static_assert(CG == 1 || (!kGA && !kGB), "CTA pairs need TMA-fed operands");
   // TMA-fed tiles leave warps 4..7 free: they join the epilogue
-  constexpr bool kEpi8 = !kGA && !kGB && BN >= 128;
+  constexpr bool kEpi8 = !kGA && !kGB;
   constexpr int kEpi = kEpi8 ? 8 : 4, kEpiWarp0 = kEpi8 ? 4 : 8;
   constexpr int kStgBufs = kEpi8 ? 1 : 2;  // 4 KB TMA-store staging buffers per warp
+  // TMA-store chunk width: 64 columns (128 B rows, 128 B swizzle), or 32 (64 B
+  // rows, 64 B swizzle) when eight warps share a 64-wide tile
+  constexpr int CW = (kEpi8 && BN == 64) ? 32 : 64;
 
   extern __shared__ uint8_t smem_raw[];
   // offset from the shared array itself (not via an integer cast), so that
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN + rank * BNL;
         // im2col A: window base of the tile's first row pixel
         int a_x = 0, a_y = 0, a_n = 0;
-        if (AM == A_IM2COL) {
+        if (AM == A_IM2COL || AM == A_IM2COL16) {
           a_x = m0 % a.gw;
           const int t = m0 / a.gw;
           a_y = t % a.gh;
@@ -250,6 +259,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             loadi2c(stA + s * C::A_BYTES, &tmA, cb * 64, a_x * a.isw + a.ilw,
                     a_y * a.ish + a.ilh, a_n, (uint16_t)sx, (uint16_t)r);
+          } else if (AM == A_IM2COL16) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // taps 4kb .. 4kb+3, 128 pixels x 32 B each
+              const int t = kb * 4 + j;
+              const int r = t / g.s, sx = t - r * g.s;
+              loadi2c(stA + s * C::A_BYTES + j * 4096, &tmA, 0, a_x, a_y, a_n, (uint16_t)sx,
+                      (uint16_t)r);
+            }
           } else if (AM == A_TMA_K) {
             load2d(stA + s * C::A_BYTES, &tmA, kb * BK, m0);
           } else if (AM == A_TMA_MN) {
@@ -268,6 +285,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < BNL / 64; ++j)
               load2d(stB + s * C::B_BYTES + j * 8192, &tmB, t * a.b_tap_stride + n0 + 64 * j,
                      kob * BK);
+          } else if (BMD == B_IM2COL16) {
+            // 64 reduction pixels x 16 channels (32 B rows) per tap, BN/16 taps
+            const int pix0 = kb * BK;
+            const int bx = pix0 % a.gw, t0 = pix0 / a.gw;
+            const int by = t0 % a.gh, bn_ = t0 / a.gh;
+#pragma unroll
+            for (int j = 0; j < BNL / 16; ++j) {
+              const int t = (n0 >> 4) + j;
+              const int r = t / g.s, sx = t - r * g.s;
+              loadi2c(stB + s * C::B_BYTES + j * 2048, &tmB, 0, bx, by, bn_, (uint16_t)sx,
+                      (uint16_t)r);
+            }
           } else if (BMD == B_IM2COL) {
             // 64 reduction pixels x 64 channels of tap (r, s) per 64-wide N block
             const int pix0 = kb * BK;
@@ -304,10 +333,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t bbase = smem_u32(stB + s * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t da = kAmn ? sdesc_sw128(abase + kk * 2048, 8192, 1024)
-                                     : sdesc_sw128(abase + kk * 32, 16, 1024);
-            const uint64_t db = kBmn ? sdesc_sw128(bbase + kk * 2048, 8192, 1024)
-                                     : sdesc_sw128(bbase + kk * 32, 16, 1024);
+            // A_IM2COL16: K step kk is tap kk's 128 x 32 B block (K-major,
+            // 32 B swizzle); B_IM2COL16: 16 pixel rows of 32 B per K step,
+            // taps (16-wide N blocks) 2 KB apart (MN-major, 32 B swizzle)
+            const uint64_t da = AM == A_IM2COL16 ? sdesc_sw32(abase + kk * 4096, 16, 256)
+                                : kAmn ? sdesc_sw128(abase + kk * 2048, 8192, 1024)
+                                       : sdesc_sw128(abase + kk * 32, 16, 1024);
+            const uint64_t db = BMD == B_IM2COL16 ? sdesc_sw32(bbase + kk * 512, 2048, 256)
+                                : kBmn ? sdesc_sw128(bbase + kk * 2048, 8192, 1024)
+                                       : sdesc_sw128(bbase + kk * 32, 16, 1024);
             if (CG == 2) mma_f16_cg2(d, da, db, IDESC, (i | kk) != 0);
             else mma_f16(d, da, db, IDESC, (i | kk) != 0);
           }
@@ -543,18 +577,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 64-column chunks: round into a 128B-swizzled 32 x 64 staging tile, TMA
         // store it (rows >= M and columns >= N are clipped by the tensor map),
         // and take the BN column sums from the staged (rounded) values.
-        for (int c = c_lo; c < c_hi; c += 64) {
-          uint32_t v[64];
+        for (int c = c_lo; c < c_hi; c += CW) {
+          uint32_t v[CW];
           const uint32_t tb = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c);
           tmem_ld32_nowait(tb, v);
-          tmem_ld32_nowait(tb + 32, v + 32);
+          if (CW == 64) tmem_ld32_nowait(tb + 32, v + 32);
           tmem_wait_ld();
           uint8_t* buf = stg + (ew * kStgBufs + (sb % kStgBufs)) * 4096;
           ++sb;
           if (lane == 0) bulk_wait_read<kStgBufs - 1>();  // buf's previous store has read it
           __syncwarp();
+          // row `lane`, 16 B piece j at the TMA swizzle position
+          const int swz = CW == 64 ? (lane & 7) : ((lane >> 1) & 3);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {  // 16 B piece j = columns c + 8j .. c + 8j + 7
+          for (int j = 0; j < CW / 8; ++j) {  // piece j = columns c + 8j .. c + 8j + 7
             uint32_t pk[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -572,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int e = 0; e < 4; ++e)
                 bad |= ((pk[e] & 0x7c00u) == 0x7c00u) | ((pk[e] & 0x7c000000u) == 0x7c000000u);
             }
-            *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+            *reinterpret_cast<uint4*>(buf + lane * (CW * 2) + ((j ^ swz) << 4)) =
                 make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
           fence_proxy_async();
@@ -581,22 +617,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_2d(&tmC, buf, n0 + c, m0 + 32 * wq);
             bulk_commit();
           }
-          if (a.stats) {  // lane owns columns c + 2*lane, c + 2*lane + 1
-            float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
+          if (a.stats) {
+            if (CW == 64) {  // lane owns columns c + 2*lane, c + 2*lane + 1
+              float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
 #pragma unroll 8
-            for (int r = 0; r < 32; ++r) {
-              const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
-                  buf + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4));
-              s1a += x.x;
-              s1b += x.y;
-              s2a += x.x * x.x;
-              s2b += x.y * x.y;
+              for (int r = 0; r < 32; ++r) {
+                const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
+                    buf + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4));
+                s1a += x.x;
+                s1b += x.y;
+                s2a += x.x * x.x;
+                s2b += x.y * x.y;
+              }
+              float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
+              rp[0] = s1a;
+              rp[1] = s2a;
+              rp[2] = s1b;
+              rp[3] = s2b;
+            } else {  // lane owns column c + lane
+              float s1 = 0.f, s2 = 0.f;
+#pragma unroll 8
+              for (int r = 0; r < 32; ++r) {
+                const float x = __half2float(*reinterpret_cast<const __half*>(
+                    buf + r * 64 + (((lane >> 3) ^ ((r >> 1) & 3)) << 4) + (lane & 7) * 2));
+                s1 += x;
+                s2 += x * x;
+              }
+              float* rp = red + ((wq * BN) + c + lane) * 2;
+              rp[0] = s1;
+              rp[1] = s2;
             }
-            float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
-            rp[0] = s1a;
-            rp[1] = s2a;
-            rp[2] = s1b;
-            rp[3] = s2b;
           }
         }
       } else
@@ -733,14 +783,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __restrict__ partial,
                                    const __half* __restrict__ bias, __half* __restrict__ out,
                                    int64_t ldc, int acc, int trans, int c4, int c4_s2,
-                                   int fr, int fs, int32_t* nonfinite) {
+                                   int fr, int fs, int s2d, int32_t* nonfinite) {
   int bad = 0;
   const int64_t total = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / N;
     int64_t n = i % N;
-    if (c4) {  // column (r, s, 4-channel slot) -> (r, s, channel); padding dropped
+    if (s2d) {  // column (block tap, 16-slot) of the space-to-depth conv -> (r, s, c)
+      const int tap = (int)(n >> 4), slot = (int)(n & 15);
+      const int br = tap / c4_s2, bc = tap - br * c4_s2;
+      const int sub = slot / c4, c = slot - sub * c4;
+      const int r = 2 * br + (sub >> 1), sx = 2 * bc + (sub & 1);
+      if (sub >= 4 || r >= fr || sx >= fs) continue;
+      n = ((int64_t)r * fs + sx) * c4 + c;
+    } else if (c4) {  // column (r, s, 4-channel slot) -> (r, s, channel); padding dropped
       const int rw = c4_s2 * 4;
       const int r = (int)(n / rw), sx = (int)(n % rw) >> 2, c = (int)(n & 3);
       if (c >= c4 || sx >= fs || r >= fr) continue;
@@ -756,6 +813,44 @@ __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __rest
     bad |= !isfinite(__half2float(h));
   }
   if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+}
+
+// space-to-depth for stride-2 narrow convolutions: xs[n][bp][bq][(sr*2+sc)*c + ch]
+// = x[n][2bp + sr - ph][2bq + sc - pw][ch] (zero outside x and in slots >= 4c)
+__global__ void k_s2d(int nimg, int h, int w, int c, int ph, int pw, int hb, int wb,
+                      const __half* __restrict__ x, uint4* __restrict__ xs) {
+  const int total = nimg * hb * wb;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int bq = i % wb, t = i / wb;
+    const int bp = t % hb, n = t / hb;
+    __align__(16) __half v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __float2half(0.f);
+    for (int sub = 0; sub < 4; ++sub) {
+      const int ih = 2 * bp + (sub >> 1) - ph, iw = 2 * bq + (sub & 1) - pw;
+      if ((unsigned)ih < (unsigned)h && (unsigned)iw < (unsigned)w) {
+        const __half* src = x + (((int64_t)n * h + ih) * w + iw) * c;
+        for (int ch = 0; ch < c; ++ch) v[sub * c + ch] = src[ch];
+      }
+    }
+    xs[2 * (int64_t)i] = reinterpret_cast<const uint4*>(v)[0];
+    xs[2 * (int64_t)i + 1] = reinterpret_cast<const uint4*>(v)[1];
+  }
+}
+
+// W[k][r][s][c] -> w2[k][(br*s2 + bc)*16 + (sr*2+sc)*c + ch] (the space-to-depth filter)
+__global__ void k_w_s2d(int k, int fr, int fs, int c, int r2, int s2, const __half* __restrict__ w,
+                        __half* __restrict__ w2) {
+  const int kp = r2 * s2 * 16, total = k * kp;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int col = i % kp, row = i / kp;
+    const int tap = col >> 4, slot = col & 15;
+    const int br = tap / s2, bc = tap - br * s2;
+    const int sub = slot / c, ch = slot - sub * c;
+    const int r = 2 * br + (sub >> 1), sx = 2 * bc + (sub & 1);
+    w2[i] = (sub < 4 && r < fr && sx < fs) ? w[(((int64_t)row * fr + r) * fs + sx) * c + ch]
+                                           : __float2half(0.f);
+  }
 }
 
 // x[n][h][w][c] (c <= 4) -> x4[n][h][w4][4]: image column w at w4 = w + off,
@@ -879,6 +974,8 @@ struct Im2colView {
   int lw = 0, lh = 0, uw = 0, uh = 0;  // bounding-box corners of the window bases
   int sw = 1, sh = 1;                  // traversal strides
   int pixels = 0;                      // pixels per load (tile rows)
+  int cbox = 64;                       // channels per pixel per load
+  int swz = 128;                       // smem swizzle of the loaded rows (128 or 32 B)
 };
 
 typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -910,8 +1007,10 @@ static int make_im2col_tmap(CUtensorMap* tm, const Im2colView& v) {
   int lower[2] = {v.lw, v.lh}, upper[2] = {v.uw, v.uh};
   cuuint32_t es[4] = {1, (cuuint32_t)v.sw, (cuuint32_t)v.sh, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(v.ptr), dims, strides,
-                   lower, upper, 64, (cuuint32_t)v.pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   lower, upper, (cuuint32_t)v.cbox, (cuuint32_t)v.pixels, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   v.swz == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
   return NNL_OK;
@@ -938,7 +1037,8 @@ static bool use_tma_store() {
   return v == 1;
 }
 
-static int make_tmap(CUtensorMap* tm, const View& v, int box_cols, int box_rows) {
+static int make_tmap(CUtensorMap* tm, const View& v, int box_cols, int box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(v.ptr) & 15) || (v.ld * 2) % 16)
@@ -948,7 +1048,7 @@ static int make_tmap(CUtensorMap* tm, const View& v, int box_cols, int box_rows)
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(v.ptr), dims, strides,
-                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return NNL_OK;
@@ -978,6 +1078,9 @@ struct Plan {
   bool c4 = false;       // narrow-channel path over a 4-channel padded copy of x
   size_t ws_x4 = 0;
   int c4_s2 = 0, c4_w4 = 0, c4_off = 0, c4_pair = 0;
+  bool s2d = false;      // stride-2 narrow conv as a stride-1 conv over a 16-channel
+  ConvGeom g2;           //   space-to-depth tensor xs with geometry g2
+  size_t ws_xs = 0;
 };
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -1062,6 +1165,31 @@ static void c4_layout(const ConvGeom& g, Plan& pl) {
   pl.ws_x4 = (size_t)g.n * g.h * pl.c4_w4 * 8;
 }
 
+// space-to-depth eligibility: stride 2, <= 4 channels (4 sub-pixels x c <= 16
+// slots), and a block filter whose taps fill whole 64-wide k-blocks
+static bool s2d_ok(const ConvGeom& g) {
+  const int r2 = (g.r + 1) / 2, s2 = (g.s + 1) / 2;
+  return !g.affine && g.sh == 2 && g.sw == 2 && g.c <= 4 && (r2 * s2) % 4 == 0 && g.k % 8 == 0;
+}
+
+static void s2d_layout(const ConvGeom& g, Plan& pl) {
+  pl.s2d = true;
+  ConvGeom v = g;
+  v.r = (g.r + 1) / 2;
+  v.s = (g.s + 1) / 2;
+  v.h = g.p + v.r - 1;
+  v.w = g.q + v.s - 1;
+  v.c = 16;
+  v.sh = v.sw = 1;
+  v.ph = v.pw = 0;
+  pl.g2 = v;
+  pl.kp = v.r * v.s * 16;
+  pl.ws_xs = (size_t)g.n * v.h * v.w * 32;
+  // im2col over xs: window bases (y, x) in [0, P) x [0, Q)
+  pl.im = {nullptr, 16, v.w, v.h, g.n, 0, 0, -(v.s - 1), -(v.r - 1), 1, 1, BM, 16, 32};
+  pl.gh = g.p; pl.gw = g.q; pl.ish = 1; pl.isw = 1; pl.ilh = 0; pl.ilw = 0;
+}
+
 static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   Plan pl;
   const ConvGeom& g = pb.g;
@@ -1104,6 +1232,12 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       } else {
         pl.amode = A_GATHER_FPROP; pl.gsrc = pb.a; pl.cblk = g.c / 64;
       }
+    } else if (s2d_ok(g) && use_tma_im2col()) {
+      s2d_layout(g, pl);
+      pl.K = pl.kp;
+      pl.amode = A_IM2COL16;
+      pl.bmode = B_TMA_K; pl.B = {nullptr, g.k, pl.kp, pl.kp};
+      pl.ws_wpad = (size_t)g.k * pl.kp * 2;
     } else if (g.c <= 4) {
       c4_layout(g, pl);
       pl.K = pl.kp;
@@ -1166,6 +1300,12 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       } else {
         pl.bmode = B_GATHER_WGRAD; pl.gsrc = pb.b; pl.cblk = g.c / 64;
       }
+    } else if (s2d_ok(g) && use_tma_im2col()) {
+      // columns in (block tap, 16-slot) order; the f32 reduction maps them back
+      s2d_layout(g, pl);
+      pl.im.pixels = 64;
+      pl.N = pl.kp;
+      pl.bmode = B_IM2COL16;
     } else if (g.c <= 4) {
       // columns in (r, s, 4-channel) order; the f32 reduction maps them back
       c4_layout(g, pl);
@@ -1226,7 +1366,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
         (pol == 2 || (pl.bn == 256 && pl.kb_per_split >= 16)))
       tile_and_split(2);
   }
-  if (pl.splits > 1 || (pl.c4 && pb.mode == kWgrad))
+  if (pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad))
     pl.ws_partial = (size_t)pl.splits * pl.M * pl.N * 4;
   pl.ok = pl.M > 0 && pl.N > 0 && pl.K > 0;
   return pl;
@@ -1286,6 +1426,8 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   NNL_TC_CASE(A_TMA_MN, B_IM2COL)
   NNL_TC_CASE(A_GATHER_C4, B_TMA_K)
   NNL_TC_CASE(A_TMA_MN, B_GATHER_C4)
+  NNL_TC_CASE(A_IM2COL16, B_TMA_K)
+  NNL_TC_CASE(A_TMA_MN, B_IM2COL16)
   if constexpr (BN >= 128) {
     NNL_TC_CASE2(A_TMA_K, B_TMA_K)
     NNL_TC_CASE2(A_TMA_K, B_TMA_MN)
@@ -1308,10 +1450,10 @@ bool tc_eligible(const GemmProblem& pb, int dtype) {
 size_t tc_ws_bytes(const GemmProblem& pb) {
   Plan pl = make_plan(pb);
   if (!pl.ok) return 0;
-  size_t w = pl.ws_im2col + pl.ws_wpad + pl.ws_partial + pl.ws_x4;
+  size_t w = pl.ws_im2col + pl.ws_wpad + pl.ws_partial + pl.ws_x4 + pl.ws_xs;
   for (int cls = 1; cls < pl.nclass; ++cls) {
     Plan q = make_plan(pb, cls);
-    const size_t v = q.ws_im2col + q.ws_wpad + q.ws_partial + q.ws_x4;
+    const size_t v = q.ws_im2col + q.ws_wpad + q.ws_partial + q.ws_x4 + q.ws_xs;
     if (v > w) w = v;
   }
   return w + 4 * 256;
@@ -1354,7 +1496,9 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   __half* wpad = nullptr;
   float* partial = nullptr;
   __half* x4 = nullptr;
+  __half* xs = nullptr;
   if (pl.ws_x4) { x4 = reinterpret_cast<__half*>(w); w = align256(w + pl.ws_x4); }
+  if (pl.ws_xs) { xs = reinterpret_cast<__half*>(w); w = align256(w + pl.ws_xs); }
   if (pl.ws_im2col) { col = reinterpret_cast<__half*>(w); w = align256(w + pl.ws_im2col); }
   if (pl.ws_wpad) { wpad = reinterpret_cast<__half*>(w); w = align256(w + pl.ws_wpad); }
   if (pl.ws_partial) partial = reinterpret_cast<float*>(w);
@@ -1366,6 +1510,22 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
                                                                           src, col);
     NNL_CHECK_LAUNCH();
     if (pb.mode == kFprop) pl.A.ptr = col; else pl.B.ptr = col;
+  }
+  if (pl.s2d) {
+    const __half* src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
+    const int64_t pix = (int64_t)g.n * pl.g2.h * pl.g2.w;
+    if (pix >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "space-to-depth input too large");
+    k_s2d<<<grid_for(pix, 256, 148 * 16), 256, 0, st>>>(g.n, g.h, g.w, g.c, g.ph, g.pw, pl.g2.h,
+                                                         pl.g2.w, src, reinterpret_cast<uint4*>(xs));
+    NNL_CHECK_LAUNCH();
+    pl.im.ptr = xs;
+    if (pb.mode == kFprop) {
+      const int total = g.k * pl.kp;
+      k_w_s2d<<<grid_for(total, 256), 256, 0, st>>>(g.k, g.r, g.s, g.c, pl.g2.r, pl.g2.s,
+                                                     reinterpret_cast<const __half*>(pb.b), wpad);
+      NNL_CHECK_LAUNCH();
+      pl.B.ptr = wpad;
+    }
   }
   if (pl.c4) {
     const __half* src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
@@ -1405,21 +1565,21 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     if ((rc = make_tmap(&ta, pl.A, 64, BM))) return rc;
   } else if (pl.amode == A_TMA_MN) {
     if ((rc = make_tmap(&ta, pl.A, 64, 64))) return rc;
-  } else if (pl.amode == A_IM2COL) {
+  } else if (pl.amode == A_IM2COL || pl.amode == A_IM2COL16) {
     if ((rc = make_im2col_tmap(&ta, pl.im))) return rc;
   }
   if (pl.bmode == B_TMA_K) {
     if ((rc = make_tmap(&tb, pl.B, 64, pl.bn / pl.cg))) return rc;
   } else if (pl.bmode == B_TMA_MN) {
     if ((rc = make_tmap(&tb, pl.B, 64, 64))) return rc;
-  } else if (pl.bmode == B_IM2COL) {
+  } else if (pl.bmode == B_IM2COL || pl.bmode == B_IM2COL16) {
     if ((rc = make_im2col_tmap(&tb, pl.im))) return rc;
   }
   TcArgs args;
   memset(&args, 0, sizeof(args));
   args.M = pl.M; args.N = pl.N; args.num_kb = pl.num_kb; args.kb_per_split = pl.kb_per_split;
   args.tiles_m = pl.tiles_m; args.tiles_n = pl.tiles_n; args.units = pl.units;
-  args.g = g;
+  args.g = pl.s2d ? pl.g2 : g;
   args.gsrc = reinterpret_cast<const __half*>(pl.gsrc);
   args.cblk = pl.cblk; args.b_kblk = pl.b_kblk; args.b_tap_stride = pl.b_tap_stride;
   args.out = pb.out; args.ldc = pl.ldc; args.acc = pb.acc; args.remap = pl.remap;
@@ -1434,7 +1594,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   args.stats = pb.stats; args.nonfinite = pb.nonfinite;
   args.K = pl.K;
   args.c4_s2 = pl.c4_s2; args.c4_w4 = pl.c4_w4; args.c4_off = pl.c4_off; args.c4_pair = pl.c4_pair;
-  const bool to_partial = pl.splits > 1 || (pl.c4 && pb.mode == kWgrad);
+  const bool to_partial = pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad);
   args.partial = to_partial ? partial : nullptr;
   if (to_partial) {  // bias / accumulate / rounding happen in the reduction
     args.bias = nullptr; args.acc = 0; args.nonfinite = nullptr; args.stats = nullptr;
@@ -1446,7 +1606,14 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
       !(reinterpret_cast<uintptr_t>(pb.out) & 15) && (pl.ldc * 2) % 16 == 0) {
     View o;
     o.ptr = pb.out; o.rows = pl.M; o.cols = pl.N; o.ld = pl.ldc;
-    if ((rc = make_tmap(&tc, o, 64, 32))) return rc;
+    // the kernel's chunk width (see CW): 32 columns when 8 epilogue warps share BN = 64
+    const bool gather = pl.amode == A_GATHER_FPROP || pl.amode == A_GATHER_DGRAD ||
+                        pl.amode == A_GATHER_C4 || pl.bmode == B_GATHER_WGRAD ||
+                        pl.bmode == B_GATHER_C4;
+    const bool cw32 = !gather && pl.bn == 64;
+    if ((rc = make_tmap(&tc, o, cw32 ? 32 : 64, 32,
+                        cw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
     args.tma_store = 1;
   }
   if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, tc, args, st);
@@ -1454,10 +1621,12 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   else rc = dispatch_bn<256>(pl, ta, tb, tc, args, st);
   if (rc) return rc;
   if (to_partial) {
-    const int c4 = pl.c4 && pb.mode == kWgrad ? g.c : 0;
+    const bool mapped = (pl.c4 || pl.s2d) && pb.mode == kWgrad;
+    const int c4 = mapped ? g.c : 0;
     k_tc_splitk_reduce<<<grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st>>>(
         pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
-        reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, c4, pl.c4_s2, g.r, g.s,
+        reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, c4,
+        pl.s2d ? pl.g2.s : pl.c4_s2, g.r, g.s, pl.s2d && pb.mode == kWgrad ? 1 : 0,
         pb.nonfinite);
     NNL_CHECK_LAUNCH();
   }

@@ -291,6 +291,17 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, ui
   return d;
 }
 
+// shared-memory matrix descriptor, 32-byte swizzle (atom: 8 rows x 32 B)
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100)
+  d |= (uint64_t)6 << 61;  // SWIZZLE_32B
+  return d;
+}
+
 // instruction descriptor: kind::f16, A/B fp16, D f32, M = 128 (or 256 for a pair)
 __host__ __device__ constexpr uint32_t idesc_f16(int n, bool a_mn, bool b_mn, int m = 128) {
   return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
