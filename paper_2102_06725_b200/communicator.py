@@ -27,9 +27,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .errors import (CollectiveTimeout, DivergedReplicas, InvalidWorkerCount,
+from .errors import (CollectiveTimeout, DivergedReplicas, InvalidWorkerCount, ShapeMismatch,
                      ShapeMismatchAcrossRanks)
-from .graph import Variable
+from .graph import Variable, _note_host_values
 from .parameters import ParameterRegistry, registry_scope
 from .solver import (DeviceLossScaler, DynamicLossScaler, SgdSolver, _device_table,
                      build_chunks, dynamic_step)
@@ -307,6 +307,21 @@ def _wire_nonfinite(loss: Variable, params: list[Variable], flag_ptr: int) -> bo
     return covered == pids
 
 
+class PendingLoss:
+    """Loss of a `step_async` step; `result()` waits for the step to finish."""
+
+    __slots__ = ("_done", "_host", "_value")
+
+    def __init__(self, done, host):
+        self._done, self._host, self._value = done, host, None
+
+    def result(self) -> float:
+        if self._value is None:
+            self._done.synchronize()
+            self._value = float(self._host[0])
+        return self._value
+
+
 class DataParallelTrainer:
     """K lock-step replicas: shard the batch, mean-all-reduce grads, update.
 
@@ -457,6 +472,68 @@ class DataParallelTrainer:
             self._work(self.replicas[0], 0, None, None, lambda r: None)
         else:
             raise NotImplementedError("step_resident needs one replica per process")
+
+    def step_async(self, x_batch: np.ndarray, label_batch: np.ndarray) -> "PendingLoss":
+        """Pipelined variant of `step` (extension, single process): the batch's
+        host->device copy runs on a copy stream into one of two staging slots, so
+        it overlaps the previous step's compute; the loss is read back
+        asynchronously into pinned memory.  `PendingLoss.result()` waits for it.
+
+        Same math as `step`: the device-side work of a step starts with the
+        import of its inputs and ends with the loss read-back.  Pass pinned host
+        arrays (e.g. `torch.empty(..., pin_memory=True).numpy()`) for an
+        asynchronous copy."""
+        if self.distributed or self.n_workers != 1:
+            raise NotImplementedError("step_async is implemented for one replica per process")
+        t = _lib.torch()
+        rep = self.replicas[0]
+        xv, lv = rep.handles["x"], rep.handles["label"]
+        feed = getattr(self, "_feed", None)
+        if feed is None:
+            dev = _lib.device()
+            feed = self._feed = {
+                "stream": t.cuda.Stream(),
+                "x": [t.empty(xv.shape, dtype=t.float32, device=dev) for _ in range(2)],
+                "t": [t.empty(lv.shape, dtype=t.float32, device=dev) for _ in range(2)],
+                "free": [None, None],   # event: the slot's import has consumed it
+                "slot": 0,
+                "loss": t.empty(1, dtype=t.float32).pin_memory(),
+                "loss_dev": t.empty(1, dtype=t.float32, device=dev),
+            }
+        x = np.asarray(x_batch, dtype=np.float32)[:self.shard_size]
+        lab = np.asarray(label_batch, dtype=np.float32)[:self.shard_size]
+        if x.shape != tuple(xv.shape) or lab.shape != tuple(lv.shape):
+            raise ShapeMismatch(f"batch shapes {x.shape}/{lab.shape} != {xv.shape}/{lv.shape}")
+        _note_host_values(lv, lab)  # label validation on the host, as `.d =` does
+        slot = feed["slot"]
+        feed["slot"] ^= 1
+        cs, main = feed["stream"], t.cuda.current_stream()
+        with t.cuda.stream(cs):
+            if feed["free"][slot] is not None:
+                cs.wait_event(feed["free"][slot])
+            hx, hl = t.from_numpy(np.ascontiguousarray(x)), t.from_numpy(np.ascontiguousarray(lab))
+            feed["x"][slot].copy_(hx, non_blocking=hx.is_pinned())
+            feed["t"][slot].copy_(hl, non_blocking=hl.is_pinned())
+            copied = t.cuda.Event()
+            copied.record(cs)
+        main.wait_event(copied)
+        xv.data.write_f32_device(feed["x"][slot])
+        lv.data.write_f32_device(feed["t"][slot])
+        free = t.cuda.Event()
+        free.record(main)
+        feed["free"][slot] = free
+        graph = getattr(self, "_graph", None)
+        if graph is not None:
+            graph.replay()
+            loss = rep.handles["loss"]
+        else:
+            loss = self._work(rep, 0, None, None, lambda r: None)
+        _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr,
+                  feed["loss_dev"].data_ptr(), _lib.stream())
+        feed["loss"].copy_(feed["loss_dev"], non_blocking=True)
+        done = t.cuda.Event()
+        done.record(main)
+        return PendingLoss(done, feed["loss"])
 
     def step(self, x_batch: np.ndarray, label_batch: np.ndarray, shard: bool = False) -> float:
         """One synchronised step; returns the batch loss (mean of shard losses).

@@ -52,10 +52,17 @@ constexpr int BM = 128, BK = 64, kThreads = 384;
 // tcgen05.mma.cta_group::2; each CTA holds its 128 rows of A and BN/2 columns
 // of B, so one k-step moves (256 + BN) x 64 operand elements through L2 for
 // 2 x 128 x BN outputs instead of 2 x (128 + BN) x 64.
-template <int BN, int CG = 1>
+// RB = 1: the whole B operand (all k-blocks of a single-N-tile GEMM, <= RES_MAX
+// bytes) stays resident in shared memory for the CTA's lifetime; the ring then
+// streams A only (weight-stationary narrow convolutions).
+constexpr int RES_MAX = 96 * 1024;
+
+template <int BN, int CG = 1, int RB = 0>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // this CTA's share of B
+  static constexpr int STAGE_B = RB ? 0 : B_BYTES;      // B bytes per ring stage
+  static constexpr int RES_BYTES = RB ? RES_MAX : 0;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int RED_BYTES = 4 * BN * 2 * 4;
   static constexpr int BIAS_BYTES = BN * 4;
@@ -63,11 +70,12 @@ struct Cfg {
   static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
   // TMA-store staging: 8 x 4 KB (4 warps x 2 buffers, or 8 warps x 1)
   static constexpr int STG_BYTES = 4 * 2 * 4096;
-  static constexpr int FIXED = 1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + STG_BYTES + 1024;
+  static constexpr int FIXED =
+      1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + STG_BYTES + 1024 + RES_BYTES;
   static constexpr int BUDGET = 232448;
-  static constexpr int STAGES_FIT = (BUDGET - FIXED) / (A_BYTES + B_BYTES);
+  static constexpr int STAGES_FIT = (BUDGET - FIXED) / (A_BYTES + STAGE_B);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int PIPE = STAGES * (A_BYTES + B_BYTES);
+  static constexpr int PIPE = STAGES * (A_BYTES + STAGE_B);
   static constexpr int SMEM = PIPE + FIXED;
   static_assert(STAGES >= 3, "pipeline too shallow");
 };
@@ -145,18 +153,19 @@ __device__ __forceinline__ void c4_chunk(uint8_t* dst, const TcArgs& a, const Co
   }
 }
 
-template <int BN, int AM, int BMD, int CG>
+template <int BN, int AM, int BMD, int CG, int RB>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const TcArgs a) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, RB>;
   constexpr int S = C::STAGES;
   constexpr int BNL = BN / CG;  // B columns held by this CTA
   constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD || AM == A_GATHER_C4;
   constexpr bool kGB = BMD == B_GATHER_WGRAD || BMD == B_GATHER_C4;
   constexpr bool kAmn = AM == A_TMA_MN;
   constexpr bool kBmn = BMD != B_TMA_K;
-  constexpr uint32_t kTmaBytes = (kGA ? 0 : C::A_BYTES) + (kGB ? 0 : C::B_BYTES);
+  constexpr uint32_t kTmaBytes = (kGA ? 0 : C::A_BYTES) + (kGB ? 0 : C::STAGE_B);
+  static_assert(!RB || (CG == 1 && !kGB), "resident B: single CTA, TMA-fed B");
   constexpr uint32_t IDESC = idesc_f16(BN, kAmn, kBmn, 128 * CG);
   static_assert(CG == 1 || (!kGA && !kGB), "CTA pairs need TMA-fed operands");
   // TMA-fed tiles leave warps 4..7 free: they join the epilogue
@@ -173,14 +182,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // [ A/B stage ring | TMA-store staging (1024-aligned) | barriers | red | bias | stats ]
   uint8_t* stA = smem;
-  uint8_t* stB = smem + S * C::A_BYTES;
-  uint8_t* stg = smem + C::PIPE;
+  uint8_t* stB = smem + S * C::A_BYTES;      // ring B stages (RB: unused)
+  uint8_t* resB = smem + C::PIPE;            // RB: all k-blocks of B
+  uint8_t* stg = smem + C::PIPE + C::RES_BYTES;
   uint8_t* misc = stg + C::STG_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(misc);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(misc + 512);  // RB: resident B landed
   float* red = reinterpret_cast<float*>(misc + 1024);
   float* bias_s = reinterpret_cast<float*>(misc + 1024 + C::RED_BYTES);
   float* stat_s = reinterpret_cast<float*>(misc + 1024 + C::RED_BYTES + C::BIAS_BYTES);
@@ -201,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kEpi * CG);
     }
+    mbar_init(bfull, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -218,6 +230,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (kTmaBytes && lane == 0) {
       int it = 0;
+      if (RB) {  // the whole B operand once (single N tile, no split)
+        mbar_arrive_tx(bfull, (uint32_t)(a.num_kb * C::B_BYTES));
+        for (int kb = 0; kb < a.num_kb; ++kb) {
+          uint8_t* dst = resB + kb * C::B_BYTES;
+          if (BMD == B_TMA_K) {
+            tma_load_2d(dst, &tmB, bfull, kb * BK, 0);
+          } else if (BMD == B_TMA_MN) {
+            int t = kb / a.b_kblk;
+            const int kob = kb - t * a.b_kblk;
+            if (a.ntap) t = a.tap_w[t];
+            else if (a.flip) t = g.r * g.s - 1 - t;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(dst + j * 8192, &tmB, bfull, t * a.b_tap_stride + 64 * j, kob * BK);
+          }
+        }
+      }
       for (int u = pair; u < a.units; u += npairs) {
         const Unit w = decode_unit(a, u);
         // this CTA's A rows and B columns of the (128*CG) x BN tile
@@ -274,7 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < BM / 64; ++j)
               load2d(stA + s * C::A_BYTES + j * 8192, &tmA, m0 + 64 * j, kb * BK);
           }
-          if (BMD == B_TMA_K) {
+          if (RB) {
+            // B is resident
+          } else if (BMD == B_TMA_K) {
             load2d(stB + s * C::B_BYTES, &tmB, kb * BK, n0);
           } else if (BMD == B_TMA_MN) {
             int t = kb / a.b_kblk;
@@ -318,6 +349,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && rank == 0) {
       int it = 0, t = 0;
+      if (RB) {
+        mbar_wait(bfull, 0);
+        tc_fence_after();
+      }
       for (int u = pair; u < a.units; u += npairs, ++t) {
         const Unit w = decode_unit(a, u);
         const int ab = t & 1;
@@ -330,7 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t abase = smem_u32(stA + s * C::A_BYTES);
-          const uint32_t bbase = smem_u32(stB + s * C::B_BYTES);
+          const uint32_t bbase = RB ? smem_u32(resB + (w.kb0 + i) * C::B_BYTES)
+                                    : smem_u32(stB + s * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             // A_IM2COL16: K step kk is tap kk's 128 x 32 B block (K-major,
@@ -1025,6 +1061,8 @@ static bool use_tma_im2col() {
   return v == 1;
 }
 
+static bool use_resident_b() { return nnl_set_tc_resident_b(-1) == 1; }
+
 // 0: never, 1: cost heuristic, 2: whenever eligible (tuning)
 static int cta_pair_policy() { return nnl_set_tc_pairs(-1); }
 
@@ -1075,6 +1113,7 @@ struct Plan {
   int splits = 1, kb_per_split = 0, num_kb = 0, tiles_m = 0, tiles_n = 0, units = 0;
   size_t ws_im2col = 0, ws_wpad = 0, ws_partial = 0;
   int cg = 1;            // 2: CTA-pair (cta_group::2) 256-row tiles
+  bool resb = false;     // B resident in shared memory (weight-stationary)
   bool c4 = false;       // narrow-channel path over a 4-channel padded copy of x
   size_t ws_x4 = 0;
   int c4_s2 = 0, c4_w4 = 0, c4_off = 0, c4_pair = 0;
@@ -1366,6 +1405,13 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
         (pol == 2 || (pl.bn == 256 && pl.kb_per_split >= 16)))
       tile_and_split(2);
   }
+  {
+    // weight-stationary: one N tile, no split, all of B within RES_MAX
+    const bool b_ok = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN;
+    const bool a_ok = pl.amode == A_TMA_K || pl.amode == A_IM2COL || pl.amode == A_IM2COL16;
+    pl.resb = use_resident_b() && b_ok && a_ok && pl.cg == 1 && pl.tiles_n == 1 &&
+            pl.splits == 1 && (int64_t)pl.num_kb * pl.bn * BK * 2 <= RES_MAX;
+  }
   if (pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad))
     pl.ws_partial = (size_t)pl.splits * pl.M * pl.N * 4;
   pl.ok = pl.M > 0 && pl.N > 0 && pl.K > 0;
@@ -1377,20 +1423,20 @@ static int plan_grid(const Plan& pl) {
   return (pl.units < pairs ? pl.units : pairs) * pl.cg;
 }
 
-template <int BN, int AM, int BMD, int CG>
+template <int BN, int AM, int BMD, int CG, int RB = 0>
 static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
                      const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
-  auto kern = k_tc_gemm<BN, AM, BMD, CG>;
+  auto kern = k_tc_gemm<BN, AM, BMD, CG, RB>;
+  using C = Cfg<BN, CG, RB>;
   static bool attr = false;
   if (!attr) {
-    NNL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg<BN, CG>::SMEM));
+    NNL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)plan_grid(pl));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Cfg<BN, CG>::SMEM;
+  cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   if (CG == 2) {
@@ -1410,8 +1456,11 @@ template <int BN>
 static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
                        const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
 #define NNL_TC_CASE(AM, BMD)                                                   \
-  if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1)                         \
+  if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1 && !pl.resb)             \
     return launch_tc<BN, AM, BMD, 1>(pl, ta, tb, tc, args, st);
+#define NNL_TC_CASE_RB(AM, BMD)                                                \
+  if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1 && pl.resb)              \
+    return launch_tc<BN, AM, BMD, 1, 1>(pl, ta, tb, tc, args, st);
 #define NNL_TC_CASE2(AM, BMD)                                                  \
   if (pl.amode == AM && pl.bmode == BMD && pl.cg == 2)                         \
     return launch_tc<BN, AM, BMD, 2>(pl, ta, tb, tc, args, st);
@@ -1428,6 +1477,11 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   NNL_TC_CASE(A_TMA_MN, B_GATHER_C4)
   NNL_TC_CASE(A_IM2COL16, B_TMA_K)
   NNL_TC_CASE(A_TMA_MN, B_IM2COL16)
+  NNL_TC_CASE_RB(A_TMA_K, B_TMA_K)
+  NNL_TC_CASE_RB(A_TMA_K, B_TMA_MN)
+  NNL_TC_CASE_RB(A_IM2COL, B_TMA_K)
+  NNL_TC_CASE_RB(A_IM2COL, B_TMA_MN)
+  NNL_TC_CASE_RB(A_IM2COL16, B_TMA_K)
   if constexpr (BN >= 128) {
     NNL_TC_CASE2(A_TMA_K, B_TMA_K)
     NNL_TC_CASE2(A_TMA_K, B_TMA_MN)
@@ -1437,6 +1491,7 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
     NNL_TC_CASE2(A_TMA_MN, B_IM2COL)
   }
 #undef NNL_TC_CASE
+#undef NNL_TC_CASE_RB
 #undef NNL_TC_CASE2
   return fail(NNL_ERR_UNSUPPORTED, "no tcgen05 kernel for mode %d/%d cg %d", pl.amode, pl.bmode,
               pl.cg);

@@ -210,3 +210,34 @@ def test_cta_pairs_match_single_cta(nnl):
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
     assert _rel_err(outs[0][2], outs[1][2]) < 2e-3
+
+
+@pytest.mark.parametrize("geom", [(64, 64, 64, 3, 1, 1, 28), (32, 64, 256, 1, 1, 0, 28),
+                                  (16, 3, 64, 7, 2, 3, 112)])
+def test_resident_b_matches_streamed(nnl, geom):
+    """Weight-stationary tiles (whole B resident in shared memory) give the same
+    bits as streaming B through the ring (fprop and dgrad need no split-K here)."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    b, cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (cout, cin, k, k)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, (cout,)).astype(np.float32)
+    outs = []
+    for resb in (1, 0):
+        prev = _lib.lib().nnl_set_tc_resident_b(resb)
+        try:
+            vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+            for v, a in zip(vs, (x, w, bias)):
+                v.d = a
+            y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+            y.forward()
+            y.backward(1.0)
+            outs.append([y.d, vs[0].g if cin % 8 == 0 else None])
+        finally:
+            _lib.lib().nnl_set_tc_resident_b(prev)
+    assert np.array_equal(outs[0][0], outs[1][0])
+    if outs[0][1] is not None:
+        assert np.array_equal(outs[0][1], outs[1][1])

@@ -233,3 +233,44 @@ def test_resnet18_cifar_step_vs_oracle(nnl, half):
         ulp = 2.0 ** -10 * np.linalg.norm(v.value) if half else 0.0  # fp16 weight rounding
         werr = np.linalg.norm(weights[k] - v.value) / (0.1 * denom + ulp)
         assert werr < 2 * tol, (k, werr)
+
+
+def test_step_async_matches_step(nnl, golden):
+    """The pipelined `step_async` (copy-stream H2D, async loss read-back) is the
+    same step as `step`: identical losses and weights, with and without a
+    captured graph."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    from paper_2102_06725_b200.communicator import DataParallelTrainer
+    g = golden("lenet")
+    _ctx(nnl, True)
+
+    def build(bs):
+        xv = nnl.Variable((bs, 1, 28, 28))
+        tv = nnl.Variable((bs,))
+        return {"x": xv, "label": tv,
+                "loss": F.softmax_cross_entropy(networks.lenet(xv, 10), tv)}
+
+    def trainer():
+        return DataParallelTrainer(1, 16, build, lr=0.05, seed=0,
+                                   loss_scaling=nnl.DynamicLossScaler(8.0, 2.0, 2000))
+
+    runs = []
+    for graph in (False, True):
+        for mode in ("sync", "async"):
+            tr = trainer()
+            losses = [tr.step(g["lenet_x"][0], g["lenet_labels"])]
+            if graph:  # (the capture runs one extra step on resident inputs, in both modes)
+                tr.capture_graph()
+            if mode == "sync":
+                losses += [tr.step(g["lenet_x"][i], g["lenet_labels"]) for i in (1, 2)]
+            else:
+                pend = [tr.step_async(g["lenet_x"][i], g["lenet_labels"]) for i in (1, 2)]
+                losses += [p.result() for p in pend]
+            runs.append((graph, losses, {k: v.d.copy() for k, v in
+                                         tr.rank0.registry.get_parameters().items()}))
+    for i in (1, 3):
+        assert runs[i][0] == runs[i - 1][0]
+        assert runs[i][1] == runs[i - 1][1]
+        for k, v in runs[i][2].items():
+            assert np.array_equal(v, runs[i - 1][2][k]), k
