@@ -497,7 +497,6 @@ class DataParallelTrainer:
                 "t": [t.empty(lv.shape, dtype=t.float32, device=dev) for _ in range(2)],
                 "free": [None, None],   # event: the slot's import has consumed it
                 "slot": 0,
-                "loss": t.empty(1, dtype=t.float32).pin_memory(),
                 "loss_dev": t.empty(1, dtype=t.float32, device=dev),
             }
         x = np.asarray(x_batch, dtype=np.float32)[:self.shard_size]
@@ -530,10 +529,11 @@ class DataParallelTrainer:
             loss = self._work(rep, 0, None, None, lambda r: None)
         _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr,
                   feed["loss_dev"].data_ptr(), _lib.stream())
-        feed["loss"].copy_(feed["loss_dev"], non_blocking=True)
+        host = t.empty(1, dtype=t.float32, pin_memory=True)  # one per pending step
+        host.copy_(feed["loss_dev"], non_blocking=True)
         done = t.cuda.Event()
         done.record(main)
-        return PendingLoss(done, feed["loss"])
+        return PendingLoss(done, host)
 
     def step(self, x_batch: np.ndarray, label_batch: np.ndarray, shard: bool = False) -> float:
         """One synchronised step; returns the batch loss (mean of shard losses).
