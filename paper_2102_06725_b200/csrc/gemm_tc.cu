@@ -347,12 +347,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && rank == 0) {
+    // The whole warp walks the loop (descriptors stay warp-uniform, in uniform
+    // registers); one elected lane issues.  Descriptors are built once per
+    // stage and advanced per 16-wide K step by adding to the address field.
+    if (rank == 0) {
       int it = 0, t = 0;
       if (RB) {
         mbar_wait(bfull, 0);
         tc_fence_after();
       }
+      // per-K16 address advance (in 16 B units) of the A and B descriptors
+      constexpr uint32_t kDA = AM == A_IM2COL16 ? 4096 / 16 : kAmn ? 2048 / 16 : 32 / 16;
+      constexpr uint32_t kDB = BMD == B_IM2COL16 ? 512 / 16 : kBmn ? 2048 / 16 : 32 / 16;
       for (int u = pair; u < a.units; u += npairs, ++t) {
         const Unit w = decode_unit(a, u);
         const int ab = t & 1;
@@ -367,25 +373,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t abase = smem_u32(stA + s * C::A_BYTES);
           const uint32_t bbase = RB ? smem_u32(resB + (w.kb0 + i) * C::B_BYTES)
                                     : smem_u32(stB + s * C::B_BYTES);
+          // A_IM2COL16: K step kk is tap kk's 128 x 32 B block (K-major,
+          // 32 B swizzle); B_IM2COL16: 16 pixel rows of 32 B per K step,
+          // taps (16-wide N blocks) 2 KB apart (MN-major, 32 B swizzle)
+          const uint64_t da0 = AM == A_IM2COL16 ? sdesc_sw32(abase, 16, 256)
+                               : kAmn ? sdesc_sw128(abase, 8192, 1024)
+                                      : sdesc_sw128(abase, 16, 1024);
+          const uint64_t db0 = BMD == B_IM2COL16 ? sdesc_sw32(bbase, 2048, 256)
+                               : kBmn ? sdesc_sw128(bbase, 8192, 1024)
+                                      : sdesc_sw128(bbase, 16, 1024);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // A_IM2COL16: K step kk is tap kk's 128 x 32 B block (K-major,
-            // 32 B swizzle); B_IM2COL16: 16 pixel rows of 32 B per K step,
-            // taps (16-wide N blocks) 2 KB apart (MN-major, 32 B swizzle)
-            const uint64_t da = AM == A_IM2COL16 ? sdesc_sw32(abase + kk * 4096, 16, 256)
-                                : kAmn ? sdesc_sw128(abase + kk * 2048, 8192, 1024)
-                                       : sdesc_sw128(abase + kk * 32, 16, 1024);
-            const uint64_t db = BMD == B_IM2COL16 ? sdesc_sw32(bbase + kk * 512, 2048, 256)
-                                : kBmn ? sdesc_sw128(bbase + kk * 2048, 8192, 1024)
-                                       : sdesc_sw128(bbase + kk * 32, 16, 1024);
-            if (CG == 2) mma_f16_cg2(d, da, db, IDESC, (i | kk) != 0);
-            else mma_f16(d, da, db, IDESC, (i | kk) != 0);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t da = da0 + (uint64_t)(kk * kDA);
+              const uint64_t db = db0 + (uint64_t)(kk * kDB);
+              if (CG == 2) mma_f16_cg2(d, da, db, IDESC, (i | kk) != 0);
+              else mma_f16(d, da, db, IDESC, (i | kk) != 0);
+            }
+            if (CG == 2) mma_commit_cg2(&empty[s]);
+            else mma_commit(&empty[s]);
           }
-          if (CG == 2) mma_commit_cg2(&empty[s]);
-          else mma_commit(&empty[s]);
+          __syncwarp();
         }
-        if (CG == 2) mma_commit_cg2(&tfull[ab]);
-        else mma_commit(&tfull[ab]);
+        if (elect_one()) {
+          if (CG == 2) mma_commit_cg2(&tfull[ab]);
+          else mma_commit(&tfull[ab]);
+        }
+        __syncwarp();
       }
     }
   } else if (!kEpi8 && warp >= 4 && warp < 8) {

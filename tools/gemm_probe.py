@@ -21,6 +21,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--shape", default="", help="M,N,K for the fwd mode (affine B x I -> O)")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--once", action="store_true")
     args = ap.parse_args()
@@ -28,6 +29,30 @@ def main():
     from paper_2102_06725_b200 import _lib
     n = args.n
     dev = torch.device("cuda")
+    if args.shape:
+        M, N, K = (int(v) for v in args.shape.split(","))
+        x = torch.randn(M, K, device=dev, dtype=torch.float16)
+        w = torch.randn(K, N, device=dev, dtype=torch.float16) * 0.01
+        out = torch.empty(M, N, device=dev, dtype=torch.float16)
+        b = torch.zeros(N, device=dev, dtype=torch.float16)
+        ws = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+        st = torch.cuda.current_stream().cuda_stream
+        fn = lambda: _lib.call("nnl_affine_fwd", 1, M, K, K, N, x.data_ptr(), w.data_ptr(),
+                               b.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), st)
+        fn()
+        ts = []
+        for _ in range(args.iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        byts = 2.0 * (M * K + K * N + M * N)
+        print(f"M={M} N={N} K={K}: {ms:8.3f} ms  {2.0 * M * N * K / ms / 1e9:8.1f} TF/s  "
+              f"{byts / ms / 1e6:8.1f} GB/s")
+        return
     x = torch.randn(n, n, device=dev, dtype=torch.float16)
     w = torch.randn(n, n, device=dev, dtype=torch.float16) * 0.01
     gy = torch.randn(n, n, device=dev, dtype=torch.float16)
