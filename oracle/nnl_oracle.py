@@ -418,6 +418,7 @@ class Model:
         self.stream = Stream(seed)
         self.half = half
         self.scope: list[str] = []
+        self.batch_stat = True  # False: BN uses the running statistics (eval graph)
 
     def param(self, path: str, shape, need_grad=True, f32=False) -> Var:
         full = "/".join(self.scope + [path])
@@ -490,7 +491,7 @@ def mlp(m: Model, x: Var, n_classes=10, hidden=(32,)) -> Var:
 
 def _conv_bn(m, x, maps, k, stride, pad, name, act):
     h = m.conv(x, maps, k, name, (stride, stride), (pad, pad))
-    h = m.bn(h, f"{name}_bn")
+    h = m.bn(h, f"{name}_bn", batch_stat=m.batch_stat)
     return m.relu(h) if act else h
 
 

@@ -473,6 +473,23 @@ class DataParallelTrainer:
         else:
             raise NotImplementedError("step_resident needs one replica per process")
 
+    def save_checkpoint(self, path: str) -> None:
+        """Parameters + solver masters/momentum + loss-scaler state of replica 0
+        (all replicas are identical) in the NNP parameter.bin record format
+        (checkpoint.py)."""
+        from . import checkpoint
+        rep = self.replicas[0]
+        scaler = rep.dscaler if rep.dscaler is not None else rep.scaler
+        checkpoint.save(path, rep.registry.get_parameters(grad_only=False), rep.solver, scaler)
+
+    def load_checkpoint(self, path: str) -> None:
+        """Restore `save_checkpoint` state into every replica, in place."""
+        from . import checkpoint
+        for rep in self.replicas:
+            scaler = rep.dscaler if rep.dscaler is not None else rep.scaler
+            checkpoint.load(path, rep.registry.get_parameters(grad_only=False), rep.solver,
+                            scaler)
+
     def step_async(self, x_batch: np.ndarray, label_batch: np.ndarray) -> "PendingLoss":
         """Pipelined variant of `step` (extension, single process): the batch's
         host->device copy runs on a copy stream into one of two staging slots, so

@@ -90,6 +90,14 @@ class DeviceLossScaler:
         raw = bytes(self._buf.cpu().numpy().tobytes())
         return bool(_lib.ScalerState.from_buffer_copy(raw).applied)
 
+    def restore(self, loss_scale: float, scaling_factor: float, interval: int,
+                counter: int) -> None:
+        """Overwrite the device state in place (checkpoint resume)."""
+        t = _lib.torch()
+        st = _lib.ScalerState(float(loss_scale), float(scaling_factor), int(interval),
+                              int(counter), 0, 1)
+        self._buf.copy_(t.frombuffer(bytearray(bytes(st)), dtype=t.uint8))
+
 
 @dataclass
 class _Slot:

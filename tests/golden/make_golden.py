@@ -259,8 +259,30 @@ def gen_mlp(nn, networks):
     return out
 
 
+def gen_nnp(nn, networks):
+    """The reference's parameter.bin bytes (nnp.py:467-481) for a half LeNet's
+    registry (F16 weights, F32 BN-free) plus an F32 record, for the checkpoint
+    format test."""
+    from nanonnl.nnp import ParameterRecord, emit_parameter_bin
+    reg = fresh(nn, True)
+    with nn.registry_scope(reg):
+        networks.lenet(nn.Variable((2, 1, 28, 28)), 10)
+    recs = [ParameterRecord(k, v.shape, v.dtype, v.d.copy(), v.need_grad)
+            for k, v in reg.get_parameters(grad_only=False).items()]
+    recs.append(ParameterRecord("extra_f32", (3,), nn.Dtype.F32,
+                                np.array([1.5, -2.25, 3e-8], np.float32), False))
+    out = {"bin": np.frombuffer(emit_parameter_bin(recs), np.uint8).copy(),
+           "names": np.array([r.name for r in recs]),
+           "f16": np.array([r.dtype is nn.Dtype.F16 for r in recs]),
+           "need_grad": np.array([r.need_grad for r in recs])}
+    for i, r in enumerate(recs):
+        out[f"v{i}"] = r.values
+    return out
+
+
 def main():
     nn, F, PF, networks, DPT = _ref()
+    np.savez_compressed(os.path.join(HERE, "nnp.npz"), **gen_nnp(nn, networks))
     np.savez_compressed(os.path.join(HERE, "numerics.npz"), **gen_numerics(nn))
     np.savez_compressed(os.path.join(HERE, "ops.npz"), **gen_ops(nn, F))
     np.savez_compressed(os.path.join(HERE, "solver.npz"), **gen_solver(nn))

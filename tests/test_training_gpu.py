@@ -274,3 +274,53 @@ def test_step_async_matches_step(nnl, golden):
         assert runs[i][1] == runs[i - 1][1]
         for k, v in runs[i][2].items():
             assert np.array_equal(v, runs[i - 1][2][k]), k
+
+
+@pytest.mark.parametrize("half", [False, True])
+def test_resnet18_eval_graph_vs_oracle(nnl, half):
+    """Eval graph (BN on running statistics, after one training step updated
+    them) and evaluate_classifier against the oracle's eval forward."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    from paper_2102_06725_b200.evaluate import evaluate_classifier
+    _ctx(nnl, half)
+    B = 4
+    x = O.uniform(1, 0, (B, 3, 32, 32), 0, 1)
+    lab = (np.arange(B) % 10).astype(np.float32)
+    xe = O.uniform(2, 0, (6, 3, 32, 32), 0, 1)   # 6 rows: a wrapped tail chunk
+    le = (np.arange(6) % 10).astype(np.float32)
+    with nnl.registry_scope(nnl.ParameterRegistry(0)) as reg:
+        xv, tv = nnl.Variable(x.shape), nnl.Variable(lab.shape)
+        loss = F.softmax_cross_entropy(networks.resnet18_cifar(xv, 10), tv)
+        solver = nnl.SgdSolver(0.1).setup(reg.get_parameters())
+        xv.d, tv.d = x, lab
+        loss.forward(clear_buffer=True)
+        loss.backward(grad_seed=8.0 if half else 1.0, clear_buffer=True)
+        if half:
+            assert nnl.dynamic_step(nnl.DynamicLossScaler(8.0, 2.0, 2000), solver).applied
+        else:
+            solver.update()
+        xe_v = nnl.Variable((B, 3, 32, 32))
+        logits = networks.resnet18_cifar(xe_v, 10, train=False)
+        err, mloss = evaluate_classifier(xe_v, logits, xe, le)
+        xe_v.d = xe[:B]
+        logits.forward()
+        got = logits.d
+    _, tr = _resnet_oracle_step(O.resnet18_cifar, x, lab, half, 0.1, 10)
+    m = tr.models[0]
+    m.batch_stat = False
+    oz = O.resnet18_cifar(m, O.Var(xe[:B], half=half), 10)
+    tol = 5e-2 if half else 1e-3
+    assert np.abs(got - oz.value).max() <= tol * max(1.0, np.abs(oz.value).max())
+    # the reference's own expressions on the oracle's logits for all 6 rows
+    rows = []
+    for start in range(0, 6, B):
+        idx = np.arange(start, start + B) % 6
+        rows.append(O.resnet18_cifar(m, O.Var(xe[idx], half=half), 10).value[:min(B, 6 - start)])
+    lg = np.concatenate(rows)
+    want_err = float((np.argmax(lg, axis=1) != le.astype(np.int64)).mean())
+    z = lg - lg.max(axis=1, keepdims=True)
+    want_loss = float(-(z - np.log(np.exp(z).sum(axis=1, keepdims=True)))[
+        np.arange(6), le.astype(np.int64)].sum()) / 6
+    assert abs(mloss - want_loss) <= tol * max(1.0, abs(want_loss))
+    assert abs(err - want_err) <= 1.0 / 6 + 1e-9  # at most one near-tie row may flip
