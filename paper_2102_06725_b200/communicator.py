@@ -269,6 +269,97 @@ class DataParallelCommunicator:
             p.unpack_mean(p.bucket.data_ptr(), world, nonfinite_ptr, stream)
 
 
+class BucketSchedule:
+    """Which gradient buckets become complete as gradients turn final.
+
+    Pure host logic (shared by the NCCL path and the gloo tests).  Buffers are
+    grouped in the order their gradients are expected to become final
+    (reverse creation order), ``plan_buckets`` style; ``ready(i)`` marks buffer
+    i final and returns the buckets it completes, ``drain()`` the ones never
+    completed (issued after backward).  Every rank derives the same schedule
+    from the same graph, so collectives are issued in the same order
+    everywhere (an NCCL requirement)."""
+
+    def __init__(self, sizes: list[int], bucket_bytes: int):
+        self.groups = plan_buckets(sizes, bucket_bytes)
+        self.bucket_of = {i: b for b, g in enumerate(self.groups) for i in g}
+        self.reset()
+
+    def reset(self) -> None:
+        self.left = [len(g) for g in self.groups]
+        self.issued = [False] * len(self.groups)
+        self.seen: set[int] = set()
+
+    def ready(self, i: int) -> list[int]:
+        if i in self.seen:
+            return []
+        self.seen.add(i)
+        b = self.bucket_of[i]
+        self.left[b] -= 1
+        if self.left[b] == 0 and not self.issued[b]:
+            self.issued[b] = True
+            return [b]
+        return []
+
+    def drain(self) -> list[int]:
+        out = [b for b in range(len(self.groups)) if not self.issued[b]]
+        for b in out:
+            self.issued[b] = True
+        return out
+
+
+class BucketedAllReduce:
+    """Gradient all_reduce overlapped with backward.
+
+    Parameters are bucketed in reverse creation order.  ``ready(v)`` (wired to
+    ``backward(on_grad_ready=...)``) is called when v's gradient is final; when
+    it completes a bucket, the communication stream waits for the compute
+    stream at that point, packs the bucket (f32), runs the NCCL sum and
+    unpacks q(sum / f32(n)) into the gradients, ORing the overflow flag —
+    while backward continues on the compute stream.  ``finish()`` issues
+    what is left and makes the compute stream wait for the communication
+    stream (the update reads the reduced gradients)."""
+
+    def __init__(self, comm: "DataParallelCommunicator", params: list[Variable],
+                 nonfinite_ptr=None, bucket_bytes: int = 8 << 20):
+        t = _lib.torch()
+        self.comm = comm
+        self.order = list(reversed(params))
+        self.index = {id(p): i for i, p in enumerate(self.order)}
+        self.schedule = BucketSchedule([p.grad.size for p in self.order], bucket_bytes)
+        self.plans = [BucketPlan([self.order[i].grad for i in g])
+                      for g in self.schedule.groups]
+        self.nonfinite_ptr = nonfinite_ptr
+        self.stream = t.cuda.Stream()
+        self.world = comm.n_workers
+        comm._validate(tuple((p.grad.shape, p.grad.dtype.value) for p in self.order))
+
+    def begin(self) -> None:
+        self.schedule.reset()
+
+    def ready(self, v: Variable) -> None:
+        i = self.index.get(id(v))
+        if i is not None:
+            for b in self.schedule.ready(i):
+                self._issue(b)
+
+    def _issue(self, b: int) -> None:
+        t = _lib.torch()
+        plan = self.plans[b]
+        self.stream.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(self.stream):
+            s = _lib.stream()
+            plan.pack(s)
+            self.comm._dist.all_reduce(plan.bucket, group=self.comm.group)
+            plan.unpack_mean(plan.bucket.data_ptr(), self.world, self.nonfinite_ptr, s)
+
+    def finish(self) -> None:
+        t = _lib.torch()
+        for b in self.schedule.drain():
+            self._issue(b)
+        t.cuda.current_stream().wait_stream(self.stream)
+
+
 MultiProcessDataParalellCommunicator = DataParallelCommunicator  # PAPER.md:88 spelling
 MultiProcessDataParallelCommunicator = DataParallelCommunicator
 
@@ -337,19 +428,24 @@ class DataParallelTrainer:
 
     def __init__(self, n_workers: int, batch_size: int, build_fn, lr: float, seed: int,
                  loss_scaling=None, clip_norm: float | None = None, timeout: float = 60.0,
-                 check_sync: bool = True, momentum: float = 0.0, weight_decay: float = 0.0):
+                 check_sync: bool = True, momentum: float = 0.0, weight_decay: float = 0.0,
+                 bucket_bytes: int = 8 << 20, distributed: bool | None = None):
         if n_workers < 1:
             raise InvalidWorkerCount(f"need at least one worker, got {n_workers}")
         if batch_size % n_workers != 0:
             raise InvalidWorkerCount(
                 f"batch size {batch_size} not divisible by {n_workers} workers")
         import torch.distributed as dist
-        self.distributed = dist.is_available() and dist.is_initialized() \
-            and dist.get_world_size() > 1
+        # ``distributed=True`` forces the process-group path even at world
+        # size 1 (tests the NCCL overlap path on a single GPU)
+        up = dist.is_available() and dist.is_initialized()
+        self.distributed = up and (dist.get_world_size() > 1 if distributed is None
+                                   else bool(distributed))
         if self.distributed and dist.get_world_size() != n_workers:
             raise InvalidWorkerCount(
                 f"n_workers={n_workers} but the process group has {dist.get_world_size()} ranks")
         self.n_workers = n_workers
+        self.bucket_bytes = bucket_bytes
         self.batch_size = batch_size
         self.shard_size = batch_size // n_workers
         self.check_sync = check_sync
@@ -397,22 +493,42 @@ class DataParallelTrainer:
             h.update(p.data.tobytes())
         return h.digest()
 
+    def _overlap(self, rep: _Replica) -> "BucketedAllReduce":
+        """The replica's bucketed all-reduce, issued from inside backward."""
+        ov = getattr(rep, "_overlap", None)
+        if ov is None:
+            flag = rep.dscaler.nonfinite_ptr if rep.dscaler is not None else None
+            ov = BucketedAllReduce(self.comm, rep.params, flag, self.bucket_bytes)
+            rep._overlap = ov
+        return ov
+
     def _work(self, rep: _Replica, rank: int, x_batch, label_batch, all_reduce) -> object:
+        """One replica step.  ``all_reduce`` is a callable run after backward,
+        or a ``BucketedAllReduce`` whose buckets are issued during backward."""
         lo = rank * self.shard_size
         if x_batch is not None:
             rep.handles["x"].d = x_batch[lo:lo + self.shard_size]
             rep.handles["label"].d = label_batch[lo:lo + self.shard_size]
         loss = rep.handles["loss"]
         loss.forward(clear_buffer=True)
+        overlap = all_reduce if isinstance(all_reduce, BucketedAllReduce) else None
+        hook = None
+        if overlap is not None:
+            overlap.begin()
+            hook = overlap.ready
         if rep.dscaler is not None:
-            loss.backward(grad_seed=rep.dscaler.loss_scale_ptr, clear_buffer=True)
+            seed = rep.dscaler.loss_scale_ptr
         elif rep.scaler is not None:
-            loss.backward(grad_seed=rep.scaler.loss_scale, clear_buffer=True)
+            seed = rep.scaler.loss_scale
         elif self.static_scale is not None:
-            loss.backward(grad_seed=self.static_scale, clear_buffer=True)
+            seed = self.static_scale
         else:
-            loss.backward(clear_buffer=True)
-        all_reduce(rep)
+            seed = 1.0
+        loss.backward(grad_seed=seed, clear_buffer=True, on_grad_ready=hook)
+        if overlap is not None:
+            overlap.finish()
+        else:
+            all_reduce(rep)
         if rep.dscaler is not None:
             rep.solver.dynamic_update(rep.dscaler, check=not self._fused_flags[id(rep)])
         elif rep.scaler is not None:
@@ -462,12 +578,7 @@ class DataParallelTrainer:
         if self.distributed:
             rep = self.replicas[0]
 
-            def ar(r):
-                flag = r.dscaler.nonfinite_ptr if r.dscaler is not None else None
-                self.comm.all_reduce([p.grad for p in r.params], division=True,
-                                     nonfinite_ptr=flag)
-
-            self._work(rep, self.ranks[0], None, None, ar)
+            self._work(rep, self.ranks[0], None, None, self._overlap(rep))
         elif self.n_workers == 1:
             self._work(self.replicas[0], 0, None, None, lambda r: None)
         else:
@@ -565,12 +676,7 @@ class DataParallelTrainer:
             x_batch = label_batch = None
             rank = self.ranks[0]
 
-            def ar(r):
-                flag = r.dscaler.nonfinite_ptr if r.dscaler is not None else None
-                self.comm.all_reduce([p.grad for p in r.params], division=True,
-                                     nonfinite_ptr=flag)
-
-            loss = self._work(rep, rank, None, None, ar)
+            loss = self._work(rep, rank, None, None, self._overlap(rep))
             t = _lib.torch()
             lv = t.empty(1, dtype=t.float32, device=_lib.device())
             _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr, lv.data_ptr(),
@@ -591,12 +697,7 @@ class DataParallelTrainer:
             rep = self.replicas[0]
             rank = self.ranks[0]
 
-            def ar(r):
-                flag = r.dscaler.nonfinite_ptr if r.dscaler is not None else None
-                self.comm.all_reduce([p.grad for p in r.params], division=True,
-                                     nonfinite_ptr=flag)
-
-            loss = self._work(rep, rank, x_batch, label_batch, ar)
+            loss = self._work(rep, rank, x_batch, label_batch, self._overlap(rep))
             t = _lib.torch()
             lv = t.empty(1, dtype=t.float32, device=_lib.device())
             _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr, lv.data_ptr(),

@@ -324,3 +324,54 @@ def test_resnet18_eval_graph_vs_oracle(nnl, half):
         np.arange(6), le.astype(np.int64)].sum()) / 6
     assert abs(mloss - want_loss) <= tol * max(1.0, abs(want_loss))
     assert abs(err - want_err) <= 1.0 / 6 + 1e-9  # at most one near-tie row may flip
+
+
+def test_overlapped_nccl_allreduce_world1_matches_local(nnl):
+    """The NCCL path with buckets issued from inside backward (forced at world
+    size 1, the only size one GPU allows) equals the purely local step bitwise:
+    the mean over one rank is q(g / 1.0) = g, so any bucket issued before its
+    gradients were final, or any gradient missed, shows up as a difference."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import networks
+    from paper_2102_06725_b200.communicator import DataParallelTrainer
+    _ctx(nnl, True)
+    B = 8
+    x = O.uniform(1, 0, (B, 3, 32, 32), 0, 1)
+    lab = (np.arange(B) % 10).astype(np.float32)
+
+    def build(bs):
+        xv = nnl.Variable((bs, 3, 32, 32))
+        tv = nnl.Variable((bs,))
+        return {"x": xv, "label": tv,
+                "loss": F.softmax_cross_entropy(networks.resnet18_cifar(xv, 10), tv)}
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        runs = []
+        for forced in (False, True):
+            tr = DataParallelTrainer(1, B, build, lr=0.1, seed=0,
+                                     loss_scaling=nnl.DynamicLossScaler(8.0, 2.0, 2000),
+                                     momentum=0.9, weight_decay=1e-4, bucket_bytes=1 << 20,
+                                     distributed=forced)
+            assert tr.distributed == forced
+            losses = [tr.step(x, lab) for _ in range(3)]
+            if forced:
+                ov = tr.rank0._overlap
+                assert len(ov.plans) > 3                  # several buckets, issued in backward
+                assert all(ov.schedule.issued)
+            runs.append((losses, {k: v.d.copy() for k, v in
+                                  tr.rank0.registry.get_parameters().items()}))
+        assert runs[0][0] == runs[1][0]
+        for k, v in runs[0][1].items():
+            assert np.array_equal(v, runs[1][1][k]), k
+    finally:
+        dist.destroy_process_group()
