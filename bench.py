@@ -53,6 +53,18 @@ def parse():
     return ap.parse_args()
 
 
+def gemm_traffic() -> dict | None:
+    """DRAM bytes of one step's tcgen05 GEMM launches from the committed ncu
+    capture (profiles/r01_traffic.json, tools/traffic_summary.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            k = json.load(f)["kernels"]["nnl::k_tc_gemm"]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"bytes_per_step": k["dram_bytes_per_launch"] * k["launches"],
+            "launches": k["launches"], "source": "profiles/r01_traffic.json (ncu dram__bytes)"}
+
+
 def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -291,6 +303,7 @@ def main():
     gemm_fl = sum(v["flops"] for k, v in prof.items())
     total_ms = sum(v["ms"] for v in prof.values())
     pk = peaks()
+    traffic = gemm_traffic()
     achieved = gemm_fl / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
 
@@ -324,7 +337,8 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "k_tc_gemm (conv/affine fwd+dgrad+wgrad)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+                     "frac": round(achieved / peak, 4) if peak else None,
+                     "traffic": (traffic or {}).get("bytes_per_step"), "traffic_detail": traffic,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "gemm_share_of_step": round(gemm_ms / total_ms, 3) if total_ms else None,
                      "gemm_tflop_per_step": round(gemm_fl / 1e12, 3)},

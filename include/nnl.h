@@ -60,6 +60,10 @@ int nnl_set_tc_pairs(int enabled);
    single-N-tile GEMMs; returns the previous setting, < 0 only queries
    (default on; env NNL_TC_RESB=0) */
 int nnl_set_tc_resident_b(int enabled);
+/* stride-2 narrow-channel convolutions (the stem) over the row-concatenated
+   64-channel space-to-depth tensor (1) or the 16-channel one (0); returns the
+   previous setting, < 0 only queries (default 1; env NNL_S2D4=0) */
+int nnl_set_tc_s2d4(int enabled);
 
 /* ---- geometry ----------------------------------------------------------- */
 typedef struct nnl_conv_shape {

@@ -888,6 +888,83 @@ __global__ void k_s2d(int nimg, int h, int w, int c, int ph, int pw, int hb, int
   }
 }
 
+// row-concatenated space-to-depth (the stem): x4[n][bp][q][bc*16 + (sr*2+sc)*c + ch]
+// = x[n][2bp + sr - ph][2(q + bc) + sc - pw][ch] for block columns bc < 4, so the
+// four block taps of one block row are one 64-channel (128 B) pixel and the
+// stride-2 convolution becomes an R/2 x 1 stride-1 convolution over 64 channels
+// (TMA im2col with 128 B rows instead of four 32 B rows per block row)
+__global__ void k_s2d4(int nimg, int h, int w, int c, int ph, int pw, int hb, int q,
+                       const __half* __restrict__ x, uint4* __restrict__ x4) {
+  const int64_t total = (int64_t)nimg * hb * q * 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int bc = (int)(i & 3);
+    const int64_t pix = i >> 2;
+    const int qq = (int)(pix % q);
+    const int64_t t = pix / q;
+    const int bp = (int)(t % hb), n = (int)(t / hb);
+    __align__(16) __half v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __float2half(0.f);
+    for (int sub = 0; sub < 4; ++sub) {
+      const int ih = 2 * bp + (sub >> 1) - ph, iw = 2 * (qq + bc) + (sub & 1) - pw;
+      if ((unsigned)ih < (unsigned)h && (unsigned)iw < (unsigned)w) {
+        const __half* src = x + (((int64_t)n * h + ih) * w + iw) * c;
+        for (int ch = 0; ch < c; ++ch) v[sub * c + ch] = src[ch];
+      }
+    }
+    x4[2 * i] = reinterpret_cast<const uint4*>(v)[0];
+    x4[2 * i + 1] = reinterpret_cast<const uint4*>(v)[1];
+  }
+}
+
+// k_s2d4 with the two input rows of a block row staged in shared memory
+// (coalesced loads; one CTA per (image, block row)); 16 B stores
+template <int C>
+__global__ void __launch_bounds__(256) k_s2d4_rows(int h, int w, int ph, int pw, int hb, int q,
+                                                   const __half* __restrict__ x,
+                                                   uint4* __restrict__ x4) {
+  extern __shared__ __half srow[];
+  const int Y = blockIdx.x % hb, n = blockIdx.x / hb;
+  const int rowh = w * C;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < 2 * rowh; i += blockDim.x) {
+    const int r = i >= rowh, j = i - r * rowh;
+    const int ih = 2 * Y + r - ph;
+    srow[i] = (unsigned)ih < (unsigned)h ? x[((int64_t)n * h + ih) * rowh + j] : __float2half(0.f);
+  }
+  __syncthreads();
+  uint4* dst = x4 + ((int64_t)n * hb + Y) * q * 8;
+  for (int i = threadIdx.x; i < q * 8; i += blockDim.x) {
+    const int chunk = i & 7, qq = i >> 3;
+    const int bc = chunk >> 1;
+    __align__(16) __half v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = __float2half(0.f);
+    if (chunk & 1) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        constexpr int kBase = 8;
+        const int slot = kBase + e, sub = slot / C, ch = slot - sub * C;
+        if (sub < 4) {
+          const int iw = 2 * (qq + bc) + (sub & 1) - pw;
+          if ((unsigned)iw < (unsigned)w) v[e] = srow[(sub >> 1) * rowh + iw * C + ch];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int sub = e / C, ch = e - sub * C;
+        if (sub < 4) {
+          const int iw = 2 * (qq + bc) + (sub & 1) - pw;
+          if ((unsigned)iw < (unsigned)w) v[e] = srow[(sub >> 1) * rowh + iw * C + ch];
+        }
+      }
+    }
+    dst[i] = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
 // W[k][r][s][c] -> w2[k][(br*s2 + bc)*16 + (sr*2+sc)*c + ch] (the space-to-depth filter)
 __global__ void k_w_s2d(int k, int fr, int fs, int c, int r2, int s2, const __half* __restrict__ w,
                         __half* __restrict__ w2) {
@@ -1134,6 +1211,8 @@ struct Plan {
   bool s2d = false;      // stride-2 narrow conv as a stride-1 conv over a 16-channel
   ConvGeom g2;           //   space-to-depth tensor xs with geometry g2
   size_t ws_xs = 0;
+  bool s2d4 = false;     //   ... or over the row-concatenated 64-channel x4 (k_s2d4)
+  int s2 = 0;            // block-tap columns per block row of the column order
 };
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -1225,21 +1304,39 @@ static bool s2d_ok(const ConvGeom& g) {
   return !g.affine && g.sh == 2 && g.sw == 2 && g.c <= 4 && (r2 * s2) % 4 == 0 && g.k % 8 == 0;
 }
 
+static bool use_s2d4() { return nnl_set_tc_s2d4(-1) == 1; }
+
 static void s2d_layout(const ConvGeom& g, Plan& pl) {
   pl.s2d = true;
   ConvGeom v = g;
   v.r = (g.r + 1) / 2;
   v.s = (g.s + 1) / 2;
   v.h = g.p + v.r - 1;
-  v.w = g.q + v.s - 1;
-  v.c = 16;
   v.sh = v.sw = 1;
   v.ph = v.pw = 0;
-  pl.g2 = v;
-  pl.kp = v.r * v.s * 16;
-  pl.ws_xs = (size_t)g.n * v.h * v.w * 32;
-  // im2col over xs: window bases (y, x) in [0, P) x [0, Q)
-  pl.im = {nullptr, 16, v.w, v.h, g.n, 0, 0, -(v.s - 1), -(v.r - 1), 1, 1, BM, 16, 32};
+  if (v.s <= 4 && use_s2d4()) {
+    // x4[n][P + R2 - 1][Q][64]: an R2 x 1 convolution over 64 channels whose
+    // reduction index (br, bc*16 + slot) is the s2d filter's with s2 = 4
+    pl.s2d4 = true;
+    pl.s2 = 4;
+    v.s = 1;
+    v.w = g.q;
+    v.c = 64;
+    pl.g2 = v;
+    pl.kp = v.r * 64;
+    pl.ws_xs = (size_t)g.n * v.h * v.w * 128;
+    pl.im = {nullptr, 64, v.w, v.h, g.n, 0, 0, 0, -(v.r - 1), 1, 1, BM, 64, 128};
+    pl.cblk = 1;
+  } else {
+    pl.s2 = v.s;
+    v.w = g.q + v.s - 1;
+    v.c = 16;
+    pl.g2 = v;
+    pl.kp = v.r * v.s * 16;
+    pl.ws_xs = (size_t)g.n * v.h * v.w * 32;
+    // im2col over xs: window bases (y, x) in [0, P) x [0, Q)
+    pl.im = {nullptr, 16, v.w, v.h, g.n, 0, 0, -(v.s - 1), -(v.r - 1), 1, 1, BM, 16, 32};
+  }
   pl.gh = g.p; pl.gw = g.q; pl.ish = 1; pl.isw = 1; pl.ilh = 0; pl.ilw = 0;
 }
 
@@ -1288,7 +1385,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     } else if (s2d_ok(g) && use_tma_im2col()) {
       s2d_layout(g, pl);
       pl.K = pl.kp;
-      pl.amode = A_IM2COL16;
+      pl.amode = pl.s2d4 ? A_IM2COL : A_IM2COL16;
       pl.bmode = B_TMA_K; pl.B = {nullptr, g.k, pl.kp, pl.kp};
       pl.ws_wpad = (size_t)g.k * pl.kp * 2;
     } else if (g.c <= 4) {
@@ -1358,7 +1455,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       s2d_layout(g, pl);
       pl.im.pixels = 64;
       pl.N = pl.kp;
-      pl.bmode = B_IM2COL16;
+      pl.bmode = pl.s2d4 ? B_IM2COL : B_IM2COL16;
     } else if (g.c <= 4) {
       // columns in (r, s, 4-channel) order; the f32 reduction maps them back
       c4_layout(g, pl);
@@ -1584,13 +1681,23 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const __half* src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
     const int64_t pix = (int64_t)g.n * pl.g2.h * pl.g2.w;
     if (pix >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "space-to-depth input too large");
-    k_s2d<<<grid_for(pix, 256, 148 * 16), 256, 0, st>>>(g.n, g.h, g.w, g.c, g.ph, g.pw, pl.g2.h,
-                                                         pl.g2.w, src, reinterpret_cast<uint4*>(xs));
+    const bool rows = pl.s2d4 && g.w * g.c * 4 <= 48 * 1024;
+#define NNL_S2D4_ROWS(CC)                                                                  \
+    if (rows && g.c == CC)                                                                 \
+      k_s2d4_rows<CC><<<g.n * pl.g2.h, 256, g.w * g.c * 4, st>>>(                          \
+          g.h, g.w, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
+    NNL_S2D4_ROWS(1) else NNL_S2D4_ROWS(2) else NNL_S2D4_ROWS(3) else NNL_S2D4_ROWS(4)
+    else if (pl.s2d4)
+      k_s2d4<<<grid_for(pix * 4, 256, 148 * 16), 256, 0, st>>>(
+          g.n, g.h, g.w, g.c, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
+    else
+      k_s2d<<<grid_for(pix, 256, 148 * 16), 256, 0, st>>>(
+          g.n, g.h, g.w, g.c, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
     NNL_CHECK_LAUNCH();
     pl.im.ptr = xs;
     if (pb.mode == kFprop) {
       const int total = g.k * pl.kp;
-      k_w_s2d<<<grid_for(total, 256), 256, 0, st>>>(g.k, g.r, g.s, g.c, pl.g2.r, pl.g2.s,
+      k_w_s2d<<<grid_for(total, 256), 256, 0, st>>>(g.k, g.r, g.s, g.c, pl.g2.r, pl.s2,
                                                      reinterpret_cast<const __half*>(pb.b), wpad);
       NNL_CHECK_LAUNCH();
       pl.B.ptr = wpad;
@@ -1695,7 +1802,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     k_tc_splitk_reduce<<<grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st>>>(
         pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
         reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, c4,
-        pl.s2d ? pl.g2.s : pl.c4_s2, g.r, g.s, pl.s2d && pb.mode == kWgrad ? 1 : 0,
+        pl.s2d ? pl.s2 : pl.c4_s2, g.r, g.s, pl.s2d && pb.mode == kWgrad ? 1 : 0,
         pb.nonfinite);
     NNL_CHECK_LAUNCH();
   }

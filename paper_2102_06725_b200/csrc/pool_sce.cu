@@ -145,6 +145,218 @@ __global__ void k_maxpool_fwd_h8(nnl_pool_shape ps, const uint4* __restrict__ x,
   }
 }
 
+// The 3x3 window reduction of 8 fp16 channels (packed, exact: the values are
+// fp16).  Fast path: m = NaN-propagating max of the window; the index is the
+// first tap equal to m and the output that tap's bits (first max wins, so
+// -0/+0 ties keep the first).  Windows with a NaN take the sequential rule
+// (NaN wins, first NaN), functions.py:255-271.
+__device__ __forceinline__ void pool9_k3(const uint4 (&u)[9], uint4& yo, uint2& a) {
+  uint32_t best[4], idx[4];
+  bool any_nan = false;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    auto word = [&](int k) -> uint32_t {
+      return q == 0 ? u[k].x : q == 1 ? u[k].y : q == 2 ? u[k].z : u[k].w;
+    };
+    uint32_t mw = word(0);
+    __half2 m = *reinterpret_cast<const __half2*>(&mw);
+#pragma unroll
+    for (int k = 1; k < 9; ++k) {
+      const uint32_t vw = word(k);
+      m = __hmax2_nan(m, *reinterpret_cast<const __half2*>(&vw));
+    }
+    const uint32_t mb = *reinterpret_cast<const uint32_t*>(&m);
+    any_nan |= ((mb & 0x7c00u) == 0x7c00u && (mb & 0x03ffu)) ||
+               ((mb & 0x7c000000u) == 0x7c000000u && (mb & 0x03ff0000u));
+    uint32_t id = 0, val = 0;
+#pragma unroll
+    for (int k = 8; k >= 0; --k) {
+      const uint32_t vw = word(k);
+      const uint32_t eq = __heq2_mask(*reinterpret_cast<const __half2*>(&vw), m);
+      id = ((uint32_t)k * 0x00010001u & eq) | (id & ~eq);
+      val = (vw & eq) | (val & ~eq);
+    }
+    best[q] = val;
+    idx[q] = id;
+  }
+  if (any_nan) {  // sequential rule, per lane
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t b = 0, id = 0, bnan = 0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const uint32_t v = q == 0 ? u[k].x : q == 1 ? u[k].y : q == 2 ? u[k].z : u[k].w;
+        const uint32_t vnan = __vcmpgtu2(v & 0x7fff7fffu, 0x7c007c00u);
+        if (k == 0) { b = v; bnan = vnan; continue; }
+        const uint32_t gt = __hgt2_mask(*reinterpret_cast<const __half2*>(&v),
+                                        *reinterpret_cast<const __half2*>(&b));
+        const uint32_t upd = gt | (vnan & ~bnan);
+        b = (v & upd) | (b & ~upd);
+        id = ((uint32_t)k * 0x00010001u & upd) | (id & ~upd);
+        bnan |= vnan;
+      }
+      best[q] = b;
+      idx[q] = id;
+    }
+  }
+  yo = make_uint4(best[0], best[1], best[2], best[3]);
+  a.x = (idx[0] & 0xffu) | ((idx[0] >> 16) << 8) | ((idx[1] & 0xffu) << 16) | ((idx[1] >> 16) << 24);
+  a.y = (idx[2] & 0xffu) | ((idx[2] >> 16) << 8) | ((idx[3] & 0xffu) << 16) | ((idx[3] >> 16) << 24);
+}
+
+// 3x3 stride-2 windows (the ResNet stem pool), fully unrolled: the nine 16 B
+// window loads of a thread are independent and issued together (the generic
+// loop above keeps one in flight), then reduced in row-major window order with
+// the same first-max / NaN-wins rule (functions.py:255-271).
+__global__ void __launch_bounds__(256) k_maxpool_fwd_k3s2(nnl_pool_shape ps,
+                                                          const uint4* __restrict__ x,
+                                                          uint4* __restrict__ y,
+                                                          uint2* __restrict__ arg) {
+  const int cg = ps.c >> 3;
+  const int total = ps.n * ps.p * ps.q * cg;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % cg;
+    int t = i / cg;
+    const int oq = t % ps.q;
+    t /= ps.q;
+    const int op = t % ps.p;
+    const int b = t / ps.p;
+    const int h0 = op * 2 - ps.ph, w0 = oq * 2 - ps.pw;
+    uint4 u[9];
+#pragma unroll
+    for (int di = 0; di < 3; ++di)
+#pragma unroll
+      for (int dj = 0; dj < 3; ++dj) {
+        const int ih = h0 + di, iw = w0 + dj;
+        u[di * 3 + dj] = (unsigned)ih < (unsigned)ps.h && (unsigned)iw < (unsigned)ps.w
+                             ? __ldg(x + ((int64_t)(b * ps.h + ih) * ps.w + iw) * cg + g)
+                             : make_uint4(0xfc00fc00u, 0xfc00fc00u, 0xfc00fc00u, 0xfc00fc00u);
+      }
+    uint4 yo;
+    uint2 a;
+    pool9_k3(u, yo, a);
+    y[i] = yo;
+    arg[i] = a;
+  }
+}
+
+// Same, one CTA per (image, output row): the three input rows of the windows
+// are staged in shared memory with coalesced 16 B loads (adjacent output rows
+// share one input row through L2), then each thread reduces windows from
+// shared memory.  Used when three input rows fit in 48 KB.
+__global__ void __launch_bounds__(256) k_maxpool_fwd_k3s2_rows(nnl_pool_shape ps,
+                                                               const uint4* __restrict__ x,
+                                                               uint4* __restrict__ y,
+                                                               uint2* __restrict__ arg) {
+  extern __shared__ uint4 rows[];
+  const int cg = ps.c >> 3, rowv = ps.w * cg;
+  const int op = blockIdx.x % ps.p, b = blockIdx.x / ps.p;
+  const int h0 = op * 2 - ps.ph;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < 3 * rowv; i += blockDim.x) {
+    const int r = i / rowv, j = i - r * rowv;
+    const int ih = h0 + r;
+    rows[i] = (unsigned)ih < (unsigned)ps.h ? __ldg(x + (int64_t)(b * ps.h + ih) * rowv + j)
+                                            : make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  // packed fp16 (exact: the values are fp16).  Fast path: m = NaN-propagating
+  // max of the window; the index is the first tap equal to m and the output
+  // that tap's bits (first max wins, so -0/+0 ties keep the first).  Windows
+  // with a NaN take the sequential rule (NaN wins, first NaN).
+  constexpr uint32_t kNegInf = 0xfc00fc00u;
+  for (int i = threadIdx.x; i < ps.q * cg; i += blockDim.x) {
+    const int g = i % cg, oq = i / cg;
+    const int w0 = oq * 2 - ps.pw;
+    uint4 u[9];
+#pragma unroll
+    for (int di = 0; di < 3; ++di) {
+      const bool rin = (unsigned)(h0 + di) < (unsigned)ps.h;
+      const uint4* rp = rows + di * rowv + g;
+#pragma unroll
+      for (int dj = 0; dj < 3; ++dj) {
+        const int iw = w0 + dj;
+        u[di * 3 + dj] = rin && (unsigned)iw < (unsigned)ps.w
+                             ? rp[iw * cg] : make_uint4(kNegInf, kNegInf, kNegInf, kNegInf);
+      }
+    }
+    uint4 yo;
+    uint2 a;
+    pool9_k3(u, yo, a);
+    const int64_t oi = ((int64_t)(b * ps.p + op) * ps.q + oq) * cg + g;
+    y[oi] = yo;
+    arg[oi] = a;
+  }
+}
+
+// Backward of the 3x3 / stride 2 / pad 1 pool: one thread per 2x2 input block
+// (2a..2a+1, 2b..2b+1) x 8 channels.  Those four pixels are only reached by
+// outputs (a..a+1, b..b+1): 4 dy + 4 index loads for 4 pixels, summed per
+// pixel in ascending output order (np.add.at order, functions.py:284-288),
+// f32, one rounding.
+__global__ void __launch_bounds__(256) k_maxpool_bwd_k3s2p1(nnl_pool_shape ps,
+                                                            const uint4* __restrict__ dy,
+                                                            const uint2* __restrict__ arg,
+                                                            uint4* __restrict__ dx, int acc) {
+  const int cg = ps.c >> 3;
+  const int hb = (ps.h + 1) >> 1, wb = (ps.w + 1) >> 1;
+  const int total = ps.n * hb * wb * cg;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % cg;
+    int t = i / cg;
+    const int bb = t % wb;
+    t /= wb;
+    const int ba = t % hb;
+    const int n = t / hb;
+    uint4 d[2][2];
+    uint2 ix[2][2];
+    bool ok[2][2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int op = ba + r, oq = bb + c;
+        ok[r][c] = op < ps.p && oq < ps.q;
+        const int64_t o = ((int64_t)(n * ps.p + op) * ps.q + oq) * cg + g;
+        d[r][c] = ok[r][c] ? __ldg(dy + o) : make_uint4(0, 0, 0, 0);
+        ix[r][c] = ok[r][c] ? __ldg(arg + o) : make_uint2(0xffffffffu, 0xffffffffu);
+      }
+#pragma unroll
+    for (int ey = 0; ey < 2; ++ey)
+#pragma unroll
+      for (int ex = 0; ex < 2; ++ex) {
+        const int ih = 2 * ba + ey, iw = 2 * bb + ex;
+        if (ih >= ps.h || iw >= ps.w) continue;
+        float s[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] = 0.f;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (r > ey) continue;  // even rows are only in window row a
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            if (c > ex) continue;
+            // window offsets of (ih, iw) inside output (ba + r, bb + c)
+            const uint32_t want = (uint32_t)((ih + 1 - 2 * (ba + r)) * 3 + (iw + 1 - 2 * (bb + c)));
+            const __half* h = reinterpret_cast<const __half*>(&d[r][c]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t word = j < 4 ? ix[r][c].x : ix[r][c].y;
+              if (((word >> (8 * (j & 3))) & 0xffu) == want) s[j] = __fadd_rn(s[j], __half2float(h[j]));
+            }
+          }
+        }
+        const int64_t o = ((int64_t)(n * ps.h + ih) * ps.w + iw) * cg + g;
+        uint4 prev = acc ? dx[o] : make_uint4(0, 0, 0, 0);
+        __half* ph = reinterpret_cast<__half*>(&prev);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          ph[j] = __float2half_rn(__fadd_rn(acc ? __half2float(ph[j]) : 0.f, s[j]));
+        dx[o] = prev;
+      }
+  }
+}
+
 __global__ void k_maxpool_bwd_h8(nnl_pool_shape ps, const uint4* __restrict__ dy,
                                  const uint2* __restrict__ arg, uint4* __restrict__ dx, int acc) {
   const int cg = ps.c >> 3;
@@ -274,8 +486,18 @@ int nnl_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x, void* y,
   if (dtype == NNL_F16 && ps->c % 8 == 0 && (int64_t)ps->n * ps->h * ps->w * ps->c < (1ll << 31) &&
       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
         reinterpret_cast<uintptr_t>(argmax)) & 15) == 0) {
-    k_maxpool_fwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
-        *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
+    const int rows_bytes = 3 * ps->w * ps->c * 2;
+    static const bool staged = getenv("NNL_POOL_ROWS") && getenv("NNL_POOL_ROWS")[0] == '1';
+    if (staged && ps->kh == 3 && ps->kw == 3 && ps->sh == 2 && ps->sw == 2 &&
+        rows_bytes <= 48 * 1024)
+      k_maxpool_fwd_k3s2_rows<<<ps->n * ps->p, 256, rows_bytes, as_stream(stream)>>>(
+          *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
+    else if (ps->kh == 3 && ps->kw == 3 && ps->sh == 2 && ps->sw == 2)
+      k_maxpool_fwd_k3s2<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+          *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
+    else
+      k_maxpool_fwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+          *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
     NNL_CHECK_LAUNCH();
     return NNL_OK;
   }
@@ -295,8 +517,15 @@ int nnl_maxpool_bwd(int dtype, const nnl_pool_shape* ps, const void* dy, const u
   if (dtype == NNL_F16 && ps->c % 8 == 0 && total < (1ll << 31) &&
       ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) |
         reinterpret_cast<uintptr_t>(argmax)) & 15) == 0) {
-    k_maxpool_bwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
-        *ps, (const uint4*)dy, (const uint2*)argmax, (uint4*)dx, accumulate);
+    if (ps->kh == 3 && ps->kw == 3 && ps->sh == 2 && ps->sw == 2 && ps->ph == 1 && ps->pw == 1)
+      k_maxpool_bwd_k3s2p1<<<grid_for((int64_t)ps->n * ((ps->h + 1) / 2) * ((ps->w + 1) / 2) *
+                                          (ps->c / 8), 256),
+                             256, 0, as_stream(stream)>>>(*ps, (const uint4*)dy,
+                                                          (const uint2*)argmax, (uint4*)dx,
+                                                          accumulate);
+    else
+      k_maxpool_bwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+          *ps, (const uint4*)dy, (const uint2*)argmax, (uint4*)dx, accumulate);
     NNL_CHECK_LAUNCH();
     return NNL_OK;
   }

@@ -85,19 +85,23 @@ def test_ops_match_reference_golden(nnl, golden):
             close(vs[j].g, g[f"{name}__g{j}"], **tol)
 
 
-def test_maxpool_indices_bit_exact_vs_oracle(nnl):
-    """Integer outputs (argmax) are bit-exact on identical inputs."""
+@pytest.mark.parametrize("shape", [(4, 8, 13, 13), (3, 24, 16, 16), (2, 16, 15, 10)])
+def test_maxpool_indices_bit_exact_vs_oracle(nnl, shape):
+    """Integer outputs (argmax) are bit-exact on identical inputs (ties from
+    half-integer values, NaN windows, odd and even extents)."""
     import paper_2102_06725_b200.functions as F
     _ctx(nnl, True)
     rng = np.random.default_rng(3)
-    x = (np.round(rng.uniform(-2, 2, (4, 8, 13, 13)) * 2) / 2).astype(np.float32)
+    x = (np.round(rng.uniform(-2, 2, shape) * 2) / 2).astype(np.float32)
     x[0, 0, 0, :4] = np.nan
     v = nnl.Variable(x.shape, need_grad=True)
     v.d = x
     y = F.max_pooling(v, (3, 3), (2, 2), pad=(1, 1))
     y.forward()
     want_y, want_arg = O.maxpool_forward(O.q16(x), (3, 3), (2, 2), (1, 1))
-    got_arg = y.parent.state["argmax"].cpu().numpy().reshape(4, 7, 7, 8).transpose(0, 3, 1, 2)
+    n, c = shape[:2]
+    got_arg = y.parent.state["argmax"].cpu().numpy().reshape(
+        n, want_arg.shape[2], want_arg.shape[3], c).transpose(0, 3, 1, 2)
     assert np.array_equal(got_arg, want_arg)
     close(y.d, O.q16(want_y), 0, 0)
     gy = O.q16(rng.uniform(-1, 1, y.shape).astype(np.float32))

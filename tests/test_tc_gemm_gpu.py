@@ -241,3 +241,34 @@ def test_resident_b_matches_streamed(nnl, geom):
     assert np.array_equal(outs[0][0], outs[1][0])
     if outs[0][1] is not None:
         assert np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("geom", [(4, 3, 64, 7, 2, 3, 40), (16, 3, 64, 7, 2, 3, 112)])
+def test_stem_s2d4_matches_s2d16(nnl, geom):
+    """The stem over the row-concatenated 64-channel space-to-depth tensor
+    (128 B im2col rows) reduces in the same (block row, block column, slot)
+    order as the 16-channel one (32 B rows): identical output and weight
+    gradient bits."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    b, cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (cout, cin, k, k)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, (cout,)).astype(np.float32)
+    outs = []
+    for mode in (1, 0):
+        prev = _lib.lib().nnl_set_tc_s2d4(mode)
+        try:
+            vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+            for v, a in zip(vs, (x, w, bias)):
+                v.d = a
+            y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+            y.forward()
+            y.backward(1.0)
+            outs.append([y.d, vs[1].g, vs[2].g])
+        finally:
+            _lib.lib().nnl_set_tc_s2d4(prev)
+    for a, c in zip(outs[0], outs[1]):
+        assert np.array_equal(a, c)
