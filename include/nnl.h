@@ -64,6 +64,10 @@ int nnl_set_tc_resident_b(int enabled);
    64-channel space-to-depth tensor (1) or the 16-channel one (0); returns the
    previous setting, < 0 only queries (default 1; env NNL_S2D4=0) */
 int nnl_set_tc_s2d4(int enabled);
+/* stride-1 convolutions over spatial pixel-box tiles (one tiled 4D TMA box per
+   filter tap) instead of TMA im2col rows: 0 off, 1 fprop + dgrad (default),
+   2 also wgrad; returns the previous setting, < 0 only queries (env NNL_TILE4) */
+int nnl_set_tc_tile4(int enabled);
 
 /* ---- geometry ----------------------------------------------------------- */
 typedef struct nnl_conv_shape {

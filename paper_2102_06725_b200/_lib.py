@@ -15,7 +15,7 @@ import threading
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnnl.so")
+LIB_PATH = os.environ.get("NNL_LIB_PATH") or os.path.join(_HERE, "libnnl.so")
 
 F32, F16 = 0, 1
 
@@ -71,6 +71,7 @@ _SIGS = {
     "nnl_set_tc_pairs": (C.c_int, [C.c_int]),
     "nnl_set_tc_resident_b": (C.c_int, [C.c_int]),
     "nnl_set_tc_s2d4": (C.c_int, [C.c_int]),
+    "nnl_set_tc_tile4": (C.c_int, [C.c_int]),
     "nnl_quantize_f16": (C.c_int, [i64, p, p, p]),
     "nnl_fill": (C.c_int, [C.c_int, i64, p, f32, p]),
     "nnl_fill_from_device": (C.c_int, [C.c_int, i64, p, p, p]),

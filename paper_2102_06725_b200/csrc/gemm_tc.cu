@@ -38,12 +38,19 @@ using namespace tc;
 // A_IM2COL16 / B_IM2COL16: stride-2 narrow-channel convolutions (the stem)
 // rewritten by space-to-depth as a stride-1 convolution over a 16-channel
 // tensor; TMA im2col with 32-byte rows, one 16-wide K step per filter tap.
+// A_TILE4 / A_TILE4MN / B_TILE4: spatial tiles.  A 128-row M tile (or a
+// 64-pixel wgrad k-block) is a (bw x bh x bi) block of output pixels, and each
+// filter tap's operand tile is ONE tiled 4D TMA box of the NHWC input shifted
+// by the tap offset (out-of-range coordinates read as zero = the padding):
+// plain tiled loads instead of per-pixel im2col rows (stride-1 convolutions
+// whose grid the box tiles exactly).
 enum AMode {
   A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4,
-  A_GATHER_C4 = 5, A_IM2COL16 = 6
+  A_GATHER_C4 = 5, A_IM2COL16 = 6, A_TILE4 = 7, A_TILE4MN = 8
 };
 enum BMode {
-  B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATHER_C4 = 4, B_IM2COL16 = 5
+  B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATHER_C4 = 4, B_IM2COL16 = 5,
+  B_TILE4 = 6
 };
 
 constexpr int BM = 128, BK = 64, kThreads = 384;
@@ -111,7 +118,20 @@ struct TcArgs {
   int32_t* nonfinite;
   float* partial;
   int tma_store;      // epilogue writes through the output tensor map (tmC)
+  // spatial tiles (A_TILE4*, B_TILE4): box (sbw x sbh x sbi) pixels, tile grid
+  // stw x sth (x fastest, then y, then image), sp_tiles boxes in all; tap
+  // (r, s) of a box at (x0, y0, n0) reads input (x0 + s + slw, y0 + r + slh, n0);
+  // the epilogue's output grid is sgw x sgh (A_TILE4: rows -> pixels, 4D store)
+  int sbw, sbh, sbi, stw, sth, sp_tiles, slw, slh, sgw, sgh;
 };
+
+// origin (x, y, image) of spatial box `tile`
+__device__ __forceinline__ void sp_origin(const TcArgs& a, int tile, int& x0, int& y0, int& n0) {
+  const int xt = tile % a.stw, t2 = tile / a.stw;
+  x0 = xt * a.sbw;
+  y0 = (t2 % a.sth) * a.sbh;
+  n0 = (t2 / a.sth) * a.sbi;
+}
 
 struct Unit {
   int tm, tn, split, kb0, nk;
@@ -162,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int BNL = BN / CG;  // B columns held by this CTA
   constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD || AM == A_GATHER_C4;
   constexpr bool kGB = BMD == B_GATHER_WGRAD || BMD == B_GATHER_C4;
-  constexpr bool kAmn = AM == A_TMA_MN;
+  constexpr bool kAmn = AM == A_TMA_MN || AM == A_TILE4MN;
   constexpr bool kBmn = BMD != B_TMA_K;
   constexpr uint32_t kTmaBytes = (kGA ? 0 : C::A_BYTES) + (kGB ? 0 : C::STAGE_B);
   static_assert(!RB || (CG == 1 && !kGB), "resident B: single CTA, TMA-fed B");
@@ -253,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN + rank * BNL;
         // im2col A: window base of the tile's first row pixel
         int a_x = 0, a_y = 0, a_n = 0;
+        if (AM == A_TILE4) sp_origin(a, m0 / BM, a_x, a_y, a_n);
         if (AM == A_IM2COL || AM == A_IM2COL16) {
           a_x = m0 % a.gw;
           const int t = m0 / a.gw;
@@ -276,6 +297,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (CG == 2) tma_load_im2col_cg2(dst, tm, fb, c, w_, h_, n_, ow, oh);
             else tma_load_im2col(dst, tm, &full[s], c, w_, h_, n_, ow, oh);
           };
+          auto load4d = [&](void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3) {
+            if (CG == 2) tma_load_4d_cg2(dst, tm, fb, c0, c1, c2, c3);
+            else tma_load_4d(dst, tm, &full[s], c0, c1, c2, c3);
+          };
+          // A_TILE4MN / B_TILE4: this k-block's pixel box
+          int kx0 = 0, ky0 = 0, kn0 = 0;
+          if (AM == A_TILE4MN || BMD == B_TILE4) sp_origin(a, kb, kx0, ky0, kn0);
           if (AM == A_IM2COL) {
             const int t = kb / a.cblk, cb = kb - t * a.cblk;
             int r, sx;
@@ -296,6 +324,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               loadi2c(stA + s * C::A_BYTES + j * 4096, &tmA, 0, a_x, a_y, a_n, (uint16_t)sx,
                       (uint16_t)r);
             }
+          } else if (AM == A_TILE4) {
+            const int t = kb / a.cblk, cb = kb - t * a.cblk;
+            const int r = t / g.s, sx = t - r * g.s;
+            load4d(stA + s * C::A_BYTES, &tmA, cb * 64, a_x + sx + a.slw, a_y + r + a.slh, a_n);
+          } else if (AM == A_TILE4MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              load4d(stA + s * C::A_BYTES + j * 8192, &tmA, m0 + 64 * j, kx0, ky0, kn0);
           } else if (AM == A_TMA_K) {
             load2d(stA + s * C::A_BYTES, &tmA, kb * BK, m0);
           } else if (AM == A_TMA_MN) {
@@ -316,6 +352,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < BNL / 64; ++j)
               load2d(stB + s * C::B_BYTES + j * 8192, &tmB, t * a.b_tap_stride + n0 + 64 * j,
                      kob * BK);
+          } else if (BMD == B_TILE4) {
+            // 64 k-block pixels x 64 channels of tap (r, s) per 64-wide N block
+#pragma unroll
+            for (int j = 0; j < BNL / 64; ++j) {
+              const int cbg = (n0 >> 6) + j;
+              const int t = cbg / a.cblk, cb = cbg - t * a.cblk;
+              const int r = t / g.s, sx = t - r * g.s;
+              load4d(stB + s * C::B_BYTES + j * 8192, &tmB, cb * 64, kx0 + sx + a.slw,
+                     ky0 + r + a.slh, kn0);
+            }
           } else if (BMD == B_IM2COL16) {
             // 64 reduction pixels x 16 channels (32 B rows) per tap, BN/16 taps
             const int pix0 = kb * BK;
@@ -615,8 +661,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int row = wq * 32 + lane;
       const int m = m0 + row;
-      const bool mv = m < a.M;
+      int ex0 = 0, ey0 = 0, en0 = 0;
+      if (AM == A_TILE4) sp_origin(a, m0 / BM, ex0, ey0, en0);
+      const bool mv = AM == A_TILE4 ? m0 / BM < a.sp_tiles : m < a.M;
       int64_t orow = m;
+      if (AM == A_TILE4) {  // tile row -> output pixel (x fastest, then y, then image)
+        const int bx = row % a.sbw, t2 = row / a.sbw;
+        orow = ((int64_t)(en0 + t2 / a.sbh) * a.sgh + ey0 + t2 % a.sbh) * a.sgw + ex0 + bx;
+      }
       if (a.remap && mv) {
         const int x = m % a.rgw, tt = m / a.rgw;
         const int y = tt % a.rgh, n = tt / a.rgh;
@@ -664,7 +716,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, buf, n0 + c, m0 + 32 * wq);
+            if (AM == A_TILE4) {  // the warp's 32 rows are a sub-box of the pixel box
+              const int rr = 32 * wq, t2 = rr / a.sbw;
+              tma_store_4d(&tmC, buf, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
+                           en0 + t2 / a.sbh);
+            } else {
+              tma_store_2d(&tmC, buf, n0 + c, m0 + 32 * wq);
+            }
             bulk_commit();
           }
           if (a.stats) {
@@ -1213,9 +1271,56 @@ struct Plan {
   size_t ws_xs = 0;
   bool s2d4 = false;     //   ... or over the row-concatenated 64-channel x4 (k_s2d4)
   int s2 = 0;            // block-tap columns per block row of the column order
+  // spatial tiles (A_TILE4 / A_TILE4MN / B_TILE4), see TcArgs
+  bool sp = false;
+  int sbw = 0, sbh = 0, sbi = 0, stw = 0, sth = 0, sp_tiles = 0, slw = 0, slh = 0;
+  int sgw = 0, sgh = 0;
+  const void* sp_a = nullptr;  // tensor of the A boxes: dims (sp_ac, sgw, sgh, n)
+  const void* sp_b = nullptr;  // wgrad B boxes: dims (sp_bc, bw_, bh_, n)
+  int sp_ac = 0, sp_bc = 0, sp_bw = 0, sp_bh = 0, sp_n = 0;
 };
 
+static bool use_tile4() { return nnl_set_tc_tile4(-1) >= 1; }
+
+static int pow2_div(int v, int cap) {
+  int p = 1;
+  while (p * 2 <= cap && v % (p * 2) == 0) p *= 2;
+  return p;
+}
+
+// a (bw x bh x bi) pixel box of `rows` pixels that tiles the (w x h x n) grid
+// exactly, with at least 4 pixels per box row group; false if none
+static bool sp_box(int w, int h, int n, int rows, Plan& pl) {
+  const int bw = pow2_div(w, rows);
+  const int bh = pow2_div(h, rows / bw);
+  const int bi = rows / (bw * bh);
+  if (bw * bh < 4 || n % bi) return false;
+  pl.sbw = bw; pl.sbh = bh; pl.sbi = bi;
+  pl.stw = w / bw; pl.sth = h / bh;
+  pl.sp_tiles = (w / bw) * (h / bh) * (n / bi);
+  return true;
+}
+
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// tiled 4D view of an NHWC fp16 tensor (dims C, W, H, N innermost first)
+static int make_tmap4(CUtensorMap* tm, const void* ptr, int c, int w, int h, int n,
+                      const int box[4], CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (c * 2) % 16)
+    return fail(NNL_ERR_UNSUPPORTED, "TMA 4D operand not 16-byte aligned");
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  cuuint32_t bx[4] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2],
+                      (cuuint32_t)box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(ptr), dims, strides,
+                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeTiled 4D failed (%d)", (int)r);
+  return NNL_OK;
+}
 
 // tile width with the smallest (waves x per-tile time) cost.  A 128 x BN
 // tile's k-step moves (128 + BN) x 64 operand elements through L2 -> SMEM,
@@ -1374,6 +1479,12 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       pl.bmode = B_TMA_K; pl.B = {pb.b, g.k, rsc, rsc};
       if (one) {
         pl.amode = A_TMA_K; pl.A = {pb.a, nhw, g.c, g.c};
+      } else if (use_tile4() && g.sh == 1 && g.sw == 1 && sp_box(g.q, g.p, g.n, BM, pl)) {
+        pl.sp = true;
+        pl.amode = A_TILE4; pl.cblk = g.c / 64;
+        pl.slw = -g.pw; pl.slh = -g.ph; pl.sgw = g.q; pl.sgh = g.p;
+        pl.sp_a = pb.a; pl.sp_ac = g.c; pl.sp_bw = g.w; pl.sp_bh = g.h; pl.sp_n = g.n;
+        pl.M = pl.sp_tiles * BM;
       } else if (use_tma_im2col()) {
         pl.amode = A_IM2COL; pl.cblk = g.c / 64;
         pl.im = {pb.a, g.c, g.w, g.h, g.n, -g.pw, -g.ph, g.pw - (g.s - 1), g.ph - (g.r - 1),
@@ -1423,6 +1534,14 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       pl.amode = A_IM2COL; pl.cblk = g.k / 64;
       pl.im = {pb.a, g.k, g.q, g.p, g.n, pl.ilw, pl.ilh, pl.gw - g.q + pl.ilw,
                pl.gh - g.p + pl.ilh, 1, 1, BM};
+    } else if (g.sh == 1 && g.sw == 1 && use_tile4() && sp_box(g.w, g.h, g.n, BM, pl)) {
+      // stride-1 dgrad over spatial tiles of dx: tap t reads dy at
+      // (x + s + pw-(S-1), y + r + ph-(R-1)) with weight tap R*S-1-t
+      pl.sp = true;
+      pl.amode = A_TILE4; pl.cblk = g.k / 64; pl.flip = 1;
+      pl.slw = g.pw - (g.s - 1); pl.slh = g.ph - (g.r - 1); pl.sgw = g.w; pl.sgh = g.h;
+      pl.sp_a = pb.a; pl.sp_ac = g.k; pl.sp_bw = g.q; pl.sp_bh = g.p; pl.sp_n = g.n;
+      pl.M = pl.sp_tiles * BM;
     } else if (g.sh == 1 && g.sw == 1 && use_tma_im2col()) {
       // stride-1 dgrad is a convolution of dy with the flipped filter:
       // dx(y,x) = sum_{r',s'} dy(y + ph-(R-1) + r', x + pw-(S-1) + s') W[R-1-r'][S-1-s']
@@ -1442,6 +1561,16 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     if (g.c % 64 == 0) {
       if (one) {
         pl.bmode = B_TMA_MN; pl.B = {pb.b, nhw, g.c, g.c};
+      } else if (nnl_set_tc_tile4(-1) == 2 && g.sh == 1 && g.sw == 1 && g.k % 64 == 0 &&
+                 sp_box(g.q, g.p, g.n, BK, pl)) {
+        // k-blocks are 64-pixel boxes of the dy grid: A = dy^T boxes, B = the
+        // tap-shifted x boxes (zero outside x)
+        pl.sp = true;
+        pl.amode = A_TILE4MN; pl.bmode = B_TILE4; pl.cblk = g.c / 64;
+        pl.slw = -g.pw; pl.slh = -g.ph;
+        pl.sp_a = pb.a; pl.sp_ac = g.k; pl.sgw = g.q; pl.sgh = g.p; pl.sp_n = g.n;
+        pl.sp_b = pb.b; pl.sp_bc = g.c; pl.sp_bw = g.w; pl.sp_bh = g.h;
+        pl.K = pl.sp_tiles * BK;
       } else if (use_tma_im2col()) {
         pl.bmode = B_IM2COL; pl.cblk = g.c / 64;
         pl.im = {pb.b, g.c, g.w, g.h, g.n, -g.pw, -g.ph, g.pw - (g.s - 1), g.ph - (g.r - 1),
@@ -1480,7 +1609,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     // split the reduction when the tile grid cannot fill the machine
     int splits = 1;
     const int sms = num_sms() / cg;  // concurrent work slots (CTAs or CTA pairs)
-    if (tiles < sms && pb.stats == nullptr && !pl.remap) {
+    if (tiles < sms && pb.stats == nullptr && !pl.remap && pl.amode != A_TILE4) {
       // wave-quantisation-aware choice: cost in k-block times of the busiest
       // slot (waves x (k-blocks per unit + epilogue)) plus the f32 partial
       // round trip of the fixed-order reduction (~0.26 us per k-block at
@@ -1509,8 +1638,10 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     // CTA pairs (256-row tiles, half the L2 operand traffic per output) pay off
     // once the k-loop is long enough for the mainloop, not the per-tile
     // epilogue, to bound the tile: 256-wide tiles with >= 16 k-blocks per unit
-    const bool a_tma = pl.amode == A_TMA_K || pl.amode == A_TMA_MN || pl.amode == A_IM2COL;
-    const bool b_tma = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN || pl.bmode == B_IM2COL;
+    const bool a_tma = pl.amode == A_TMA_K || pl.amode == A_TMA_MN || pl.amode == A_IM2COL ||
+                       pl.amode == A_TILE4 || pl.amode == A_TILE4MN;
+    const bool b_tma = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN || pl.bmode == B_IM2COL ||
+                       pl.bmode == B_TILE4;
     const int pol = cta_pair_policy();
     if (pol && a_tma && b_tma && pl.bn >= 128 && pl.M > BM &&
         (pol == 2 || (pl.bn == 256 && pl.kb_per_split >= 16)))
@@ -1519,7 +1650,8 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   {
     // weight-stationary: one N tile, no split, all of B within RES_MAX
     const bool b_ok = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN;
-    const bool a_ok = pl.amode == A_TMA_K || pl.amode == A_IM2COL || pl.amode == A_IM2COL16;
+    const bool a_ok = pl.amode == A_TMA_K || pl.amode == A_IM2COL || pl.amode == A_IM2COL16 ||
+                      pl.amode == A_TILE4;
     pl.resb = use_resident_b() && b_ok && a_ok && pl.cg == 1 && pl.tiles_n == 1 &&
             pl.splits == 1 && (int64_t)pl.num_kb * pl.bn * BK * 2 <= RES_MAX;
   }
@@ -1588,6 +1720,11 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   NNL_TC_CASE(A_TMA_MN, B_GATHER_C4)
   NNL_TC_CASE(A_IM2COL16, B_TMA_K)
   NNL_TC_CASE(A_TMA_MN, B_IM2COL16)
+  NNL_TC_CASE(A_TILE4, B_TMA_K)
+  NNL_TC_CASE(A_TILE4, B_TMA_MN)
+  NNL_TC_CASE(A_TILE4MN, B_TILE4)
+  NNL_TC_CASE_RB(A_TILE4, B_TMA_K)
+  NNL_TC_CASE_RB(A_TILE4, B_TMA_MN)
   NNL_TC_CASE_RB(A_TMA_K, B_TMA_K)
   NNL_TC_CASE_RB(A_TMA_K, B_TMA_MN)
   NNL_TC_CASE_RB(A_IM2COL, B_TMA_K)
@@ -1600,6 +1737,9 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
     NNL_TC_CASE2(A_IM2COL, B_TMA_K)
     NNL_TC_CASE2(A_IM2COL, B_TMA_MN)
     NNL_TC_CASE2(A_TMA_MN, B_IM2COL)
+    NNL_TC_CASE2(A_TILE4, B_TMA_K)
+    NNL_TC_CASE2(A_TILE4, B_TMA_MN)
+    NNL_TC_CASE2(A_TILE4MN, B_TILE4)
   }
 #undef NNL_TC_CASE
 #undef NNL_TC_CASE_RB
@@ -1737,14 +1877,23 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   memset(&ta, 0, sizeof(ta));
   memset(&tb, 0, sizeof(tb));
   int rc;
-  if (pl.amode == A_TMA_K) {
+  if (pl.amode == A_TILE4) {
+    const int box[4] = {64, pl.sbw, pl.sbh, pl.sbi};
+    if ((rc = make_tmap4(&ta, pl.sp_a, pl.sp_ac, pl.sp_bw, pl.sp_bh, pl.sp_n, box))) return rc;
+  } else if (pl.amode == A_TILE4MN) {
+    const int box[4] = {64, pl.sbw, pl.sbh, pl.sbi};
+    if ((rc = make_tmap4(&ta, pl.sp_a, pl.sp_ac, pl.sgw, pl.sgh, pl.sp_n, box))) return rc;
+  } else if (pl.amode == A_TMA_K) {
     if ((rc = make_tmap(&ta, pl.A, 64, BM))) return rc;
   } else if (pl.amode == A_TMA_MN) {
     if ((rc = make_tmap(&ta, pl.A, 64, 64))) return rc;
   } else if (pl.amode == A_IM2COL || pl.amode == A_IM2COL16) {
     if ((rc = make_im2col_tmap(&ta, pl.im))) return rc;
   }
-  if (pl.bmode == B_TMA_K) {
+  if (pl.bmode == B_TILE4) {
+    const int box[4] = {64, pl.sbw, pl.sbh, pl.sbi};
+    if ((rc = make_tmap4(&tb, pl.sp_b, pl.sp_bc, pl.sp_bw, pl.sp_bh, pl.sp_n, box))) return rc;
+  } else if (pl.bmode == B_TMA_K) {
     if ((rc = make_tmap(&tb, pl.B, 64, pl.bn / pl.cg))) return rc;
   } else if (pl.bmode == B_TMA_MN) {
     if ((rc = make_tmap(&tb, pl.B, 64, 64))) return rc;
@@ -1769,6 +1918,9 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   args.bias = reinterpret_cast<const __half*>(pb.bias);
   args.stats = pb.stats; args.nonfinite = pb.nonfinite;
   args.K = pl.K;
+  args.sbw = pl.sbw; args.sbh = pl.sbh; args.sbi = pl.sbi; args.stw = pl.stw; args.sth = pl.sth;
+  args.sp_tiles = pl.sp_tiles; args.slw = pl.slw; args.slh = pl.slh;
+  args.sgw = pl.sgw; args.sgh = pl.sgh;
   args.c4_s2 = pl.c4_s2; args.c4_w4 = pl.c4_w4; args.c4_off = pl.c4_off; args.c4_pair = pl.c4_pair;
   const bool to_partial = pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad);
   args.partial = to_partial ? partial : nullptr;
@@ -1787,9 +1939,15 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
                         pl.amode == A_GATHER_C4 || pl.bmode == B_GATHER_WGRAD ||
                         pl.bmode == B_GATHER_C4;
     const bool cw32 = !gather && pl.bn == 64;
-    if ((rc = make_tmap(&tc, o, cw32 ? 32 : 64, 32,
-                        cw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B)))
+    const CUtensorMapSwizzle sw = cw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+    if (pl.amode == A_TILE4) {  // 32-row sub-boxes of the pixel box over the output grid
+      const int bw32 = pl.sbw < 32 ? pl.sbw : 32;
+      const int bh32 = pl.sbh < 32 / bw32 ? pl.sbh : 32 / bw32;
+      const int box[4] = {cw32 ? 32 : 64, bw32, bh32, 32 / (bw32 * bh32)};
+      if ((rc = make_tmap4(&tc, pb.out, pl.N, pl.sgw, pl.sgh, pl.sp_n, box, sw))) return rc;
+    } else if ((rc = make_tmap(&tc, o, cw32 ? 32 : 64, 32, sw))) {
       return rc;
+    }
     args.tma_store = 1;
   }
   if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, tc, args, st);
