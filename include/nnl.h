@@ -130,6 +130,33 @@ int nnl_conv2d_bwd_weight(const nnl_conv_shape* cs, int dtype, const void* x, co
 /* number of stat-partial rows nnl_conv2d_fwd writes (0 if fusion unsupported) */
 int32_t nnl_conv2d_stat_rows(const nnl_conv_shape* cs, int dtype);
 
+/* Backward-data of the convolution that consumes a BatchNormalization[+ReLU]
+   output, with the BN backward's statistics pass fused into the epilogue
+   (extension of functions.py:418-422; replaces the separate reduction pass of
+   nnl_bn_bwd).  g = the convolution's input gradient exactly as
+   nnl_conv2d_bwd_data writes it (q(prev + .) when accumulate); then
+   gy = g * gate with gate = (gate > 0) (residual tail: gate is the ReLU output
+   after the Add2) or (q(gamma*xhat + beta) > 0) (relu: fused BN->ReLU), and
+   xhat = (x - save_mean) * save_istd.  Writes q(gy) (canonical: q(0 + gy)) to
+   out (NULL: dx) and per-CTA column sums (gy, gy*xhat) to partials
+   [nnl_conv2d_bwd_data_bn_rows][2][C], which nnl_bn_bwd_apply consumes. */
+typedef struct nnl_bn_bwd_fuse {
+  const void* x;               /* BN input, NHWC like dx */
+  const void* gate;            /* nullable: residual-tail ReLU output */
+  const float* gamma;          /* relu: BN gamma / beta */
+  const float* beta;
+  const float* save_mean;      /* forward batch statistics */
+  const float* save_istd;
+  int32_t relu;
+  int32_t canonical;
+  void* out;                   /* nullable: gated gradient destination */
+  float* partials;
+} nnl_bn_bwd_fuse;
+int32_t nnl_conv2d_bwd_data_bn_rows(const nnl_conv_shape* cs, int dtype);
+int nnl_conv2d_bwd_data_bn(const nnl_conv_shape* cs, int dtype, const void* dy, const void* w,
+                           void* dx, int accumulate, const nnl_bn_bwd_fuse* bf, void* ws,
+                           size_t ws_bytes, void* stream);
+
 /* ---- MaxPooling: functions.py:217-291 ----------------------------------- */
 int nnl_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x, void* y,
                     uint8_t* argmax, void* stream);
@@ -195,6 +222,15 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
                void* dx, int acc_x, float* dgamma, int acc_g, float* dbeta, int acc_b,
                void* conv_bias_grad, int acc_cb,
                int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
+/* nnl_bn_bwd when the statistics pass already ran in the producing dgrad's
+   epilogue (nnl_conv2d_bwd_data_bn): gy is the gated gradient, partials its
+   [nparts][2][c] column sums (gy, gy*xhat); finalize + apply only. */
+int nnl_bn_bwd_apply(int dtype, int64_t rows, int32_t c, const void* x, const void* gy,
+                     const float* partials, int32_t nparts, const float* gamma,
+                     const float* save_mean, const float* save_istd, int batch_stat,
+                     void* dx, int acc_x, float* dgamma, int acc_g, float* dbeta, int acc_b,
+                     void* conv_bias_grad, int acc_cb, int32_t* nonfinite, void* ws,
+                     size_t ws_bytes, void* stream);
 
 /* ---- Solver: solver.py:67-164 ------------------------------------------- */
 typedef struct nnl_param_slot {

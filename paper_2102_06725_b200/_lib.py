@@ -49,6 +49,13 @@ class PoolShape(C.Structure):
                                    "p", "q")]
 
 
+class BnBwdFuse(C.Structure):
+    """nnl_bn_bwd_fuse (include/nnl.h)."""
+    _fields_ = [("x", p), ("gate", p), ("gamma", p), ("beta", p), ("save_mean", p),
+                ("save_istd", p), ("relu", i32), ("canonical", i32), ("out", p),
+                ("partials", p)]
+
+
 class ParamSlot(C.Structure):
     _fields_ = [("data", p), ("grad", p), ("master", p), ("momentum", p), ("n", i64),
                 ("dtype", i32), ("pad_", i32)]
@@ -88,6 +95,8 @@ _SIGS = {
     "nnl_conv2d_fwd": (C.c_int, [p, C.c_int, p, p, p, p, p, p, sz, p]),
     "nnl_conv2d_bwd_data": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, sz, p]),
     "nnl_conv2d_bwd_weight": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, C.c_int, p, p, sz, p]),
+    "nnl_conv2d_bwd_data_bn_rows": (i32, [p, C.c_int]),
+    "nnl_conv2d_bwd_data_bn": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, p, sz, p]),
     "nnl_maxpool_fwd": (C.c_int, [C.c_int, p, p, p, p, p]),
     "nnl_maxpool_bwd": (C.c_int, [C.c_int, p, p, p, p, C.c_int, p]),
     "nnl_relu_fwd": (C.c_int, [C.c_int, i64, p, p, p]),
@@ -105,6 +114,8 @@ _SIGS = {
     "nnl_bn_bwd": (C.c_int, [C.c_int, i64, i32, p, p, C.c_int, p, p, C.c_int, p, p, p, p,
                              C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, sz,
                              p]),
+    "nnl_bn_bwd_apply": (C.c_int, [C.c_int, i64, i32, p, p, p, i32, p, p, p, C.c_int, p,
+                                   C.c_int, p, C.c_int, p, C.c_int, p, C.c_int, p, p, sz, p]),
     "nnl_multi_nonfinite": (C.c_int, [p, p, i32, p, p]),
     "nnl_multi_scale_grad": (C.c_int, [p, p, i32, f32, p]),
     "nnl_multi_sumsq": (C.c_int, [p, p, i32, p, p]),

@@ -732,4 +732,40 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
   return NNL_OK;
 }
 
+int nnl_bn_bwd_apply(int dtype, int64_t rows, int32_t c, const void* x, const void* gy,
+                     const float* partials, int32_t nparts, const float* gamma,
+                     const float* save_mean, const float* save_istd, int batch_stat,
+                     void* dx, int acc_x, float* dgamma, int acc_g, float* dbeta, int acc_b,
+                     void* conv_bias_grad, int acc_cb, int32_t* nonfinite, void* ws,
+                     size_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (ws_bytes < bn_ws_bytes(rows, c))
+    return fail(NNL_ERR_INVALID_ARGUMENT, "bn workspace too small");
+  if (!partials || nparts <= 0) return fail(NNL_ERR_INVALID_ARGUMENT, "no statistics partials");
+  if (!use_stream(dtype, rows, c, x, gy, dx))
+    return fail(NNL_ERR_UNSUPPORTED, "bn_bwd_apply needs the streaming layout");
+  const int64_t bx = bn_stream_rows(BNS_STATS_B, 2, rows, c);
+  float* gsum = (float*)ws + bx * 2 * c;
+  float* bparts = gsum + 2 * c;
+  k_bn_finalize_bwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+      partials, nparts, c, gsum, dgamma, acc_g, dbeta, acc_b, nonfinite);
+  NNL_CHECK_LAUNCH();
+  if (!dx) return NNL_OK;
+  float* bp = conv_bias_grad ? bparts : nullptr;
+  BnStreamArgs a = {};
+  a.rows = rows; a.c = c; a.x = (const __half*)x; a.out = (__half*)dx; a.dy = (const __half*)gy;
+  a.gamma = gamma; a.mu = save_mean; a.istd = save_istd; a.gsum = gsum;
+  a.partials = bp; a.relu = 0; a.acc = acc_x; a.batch_stat = batch_stat;
+  a.reverse = 1;  // the dgrad epilogue wrote gy first to last
+  int rc = bn_stream_launch(BNS_APPLY_B, a, st);
+  if (rc) return rc;
+  if (bp) {
+    const int32_t brows = bn_stream_rows(BNS_APPLY_B, bn_stream_nt(BNS_APPLY_B, a), rows, c);
+    k_bn_bias_finalize<__half><<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+        bp, brows, c, (__half*)conv_bias_grad, acc_cb, nonfinite);
+    NNL_CHECK_LAUNCH();
+  }
+  return NNL_OK;
+}
+
 }  // extern "C"

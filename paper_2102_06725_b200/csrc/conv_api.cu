@@ -81,6 +81,33 @@ int nnl_conv2d_bwd_data(const nnl_conv_shape* cs, int dtype, const void* dy, con
   return run_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
 }
 
+int32_t nnl_conv2d_bwd_data_bn_rows(const nnl_conv_shape* cs, int dtype) {
+  if (check_conv(cs)) return 0;
+  GemmProblem pb = conv_problem(cs, kDgrad);
+  if (!g_tc_enabled || !tc_eligible(pb, dtype)) return 0;
+  return tc_bnb_rows(pb, dtype);
+}
+
+int nnl_conv2d_bwd_data_bn(const nnl_conv_shape* cs, int dtype, const void* dy, const void* w,
+                           void* dx, int accumulate, const nnl_bn_bwd_fuse* bf, void* ws,
+                           size_t ws_bytes, void* stream) {
+  int rc = check_conv(cs);
+  if (rc) return rc;
+  if (!bf || !bf->x || !bf->save_mean || !bf->save_istd || !bf->partials)
+    return fail(NNL_ERR_INVALID_ARGUMENT, "incomplete BN-backward fusion descriptor");
+  if (bf->relu && (bf->gate || !bf->gamma || !bf->beta))
+    return fail(NNL_ERR_INVALID_ARGUMENT, "fused ReLU needs gamma/beta and no gate");
+  GemmProblem pb = conv_problem(cs, kDgrad);
+  if (!g_tc_enabled || !tc_eligible(pb, dtype) || tc_bnb_rows(pb, dtype) == 0)
+    return fail(NNL_ERR_UNSUPPORTED, "BN-backward statistics epilogue not available");
+  pb.a = dy; pb.b = w; pb.out = dx; pb.acc = accumulate;
+  pb.stats = bf->partials;
+  pb.bnx = bf->x; pb.bn_gate = bf->gate; pb.bn_mean = bf->save_mean; pb.bn_istd = bf->save_istd;
+  pb.bn_gamma = bf->gamma; pb.bn_beta = bf->beta; pb.bn_relu = bf->relu;
+  pb.bn_canon = bf->canonical; pb.bn_out = bf->out;
+  return tc_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
+}
+
 int nnl_conv2d_bwd_weight(const nnl_conv_shape* cs, int dtype, const void* x, const void* dy,
                           void* dw, int acc_w, void* db, int acc_b, int32_t* nonfinite, void* ws,
                           size_t ws_bytes, void* stream) {

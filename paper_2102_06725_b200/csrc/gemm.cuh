@@ -38,6 +38,12 @@ struct GemmProblem {
   int out_trans;       // write D[m][n] at n*M + m (affine wgrad)
   int32_t* nonfinite;  // nullable
   float* stats;        // fprop BN partials [ceil(M/128)][2][N], nullable
+  // dgrad with the following BN's backward statistics fused (TcArgs::bnx ...)
+  const void* bnx = nullptr;
+  const void* bn_gate = nullptr;
+  const float *bn_mean = nullptr, *bn_istd = nullptr, *bn_gamma = nullptr, *bn_beta = nullptr;
+  int bn_relu = 0, bn_canon = 0;
+  void* bn_out = nullptr;
 };
 
 inline ConvGeom make_geom(const nnl_conv_shape& cs) {
@@ -74,6 +80,8 @@ int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStr
 size_t tc_ws_bytes(const GemmProblem& pb);
 bool tc_eligible(const GemmProblem& pb, int dtype);
 int32_t tc_stat_rows(const GemmProblem& pb, int dtype);
+// partial rows of a dgrad with fused BN-backward statistics (0: unsupported)
+int32_t tc_bnb_rows(const GemmProblem& pb, int dtype);
 // column sums of dy (bias gradient, functions.py:116,212): db[n] = q(prev + sum_m dy[m][n])
 int bias_grad(int dtype, int64_t rows, int64_t cols, const void* dy, void* db, int acc,
               int32_t* nonfinite, void* ws, size_t ws_bytes, cudaStream_t st);

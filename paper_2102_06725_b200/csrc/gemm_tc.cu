@@ -72,7 +72,7 @@ struct Cfg {
   static constexpr int RES_BYTES = RB ? RES_MAX : 0;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int RED_BYTES = 4 * BN * 2 * 4;
-  static constexpr int BIAS_BYTES = BN * 4;
+  static constexpr int BIAS_BYTES = BN * 4 * 5;  // bias + the fused BN-backward constants
   static constexpr int MAX_STAT_N = 2048;  // per-CTA BN statistics accumulator [2][N]
   static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
   // TMA-store staging: 8 x 4 KB (4 warps x 2 buffers, or 8 warps x 1)
@@ -123,6 +123,16 @@ struct TcArgs {
   // (r, s) of a box at (x0, y0, n0) reads input (x0 + s + slw, y0 + r + slh, n0);
   // the epilogue's output grid is sgw x sgh (A_TILE4: rows -> pixels, 4D store)
   int sbw, sbh, sbi, stw, sth, sp_tiles, slw, slh, sgw, sgh;
+  // fused BatchNormalization backward statistics (dgrad of the convolution
+  // after a BN[+ReLU]): g = the rounded dgrad output; gy = g * gate with gate
+  // = (bn_gate > 0) (residual tail) or (q(gamma*xhat + beta) > 0) (bn_relu),
+  // xhat = (bnx - mean) * istd; writes q(gy) (bn_canon: q(0 + gy)) to bn_out
+  // and per-CTA column sums (gy, gy*xhat) to stats (functions.py:418-422)
+  const __half* bnx;
+  const __half* bn_gate;
+  const float *bn_mean, *bn_istd, *bn_gamma, *bn_beta;
+  int bn_relu, bn_canon;
+  __half* bn_out;
 };
 
 // origin (x, y, image) of spatial box `tile`
@@ -173,7 +183,9 @@ __device__ __forceinline__ void c4_chunk(uint8_t* dst, const TcArgs& a, const Co
   }
 }
 
-template <int BN, int AM, int BMD, int CG, int RB>
+// EP = 1: the fused BN-backward statistics epilogue (TcArgs::bnx); a separate
+// instantiation so the common epilogue keeps its register budget
+template <int BN, int AM, int BMD, int CG, int RB, int EP>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const TcArgs a) {
@@ -651,14 +663,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit w = decode_unit(a, u);
       const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN;
       const int ab = t & 1;
-      if (a.bias) {  // this tile's bias slice, staged once in shared memory (as f32)
+      if (a.bias || EP == 1) {  // this tile's bias / BN slices, staged once (as f32)
         named_sync(2, kEpiThreads);
-        for (int j = tid; j < BN; j += kEpiThreads)
-          bias_s[j] = n0 + j < a.N ? __half2float(a.bias[n0 + j]) : 0.f;
+        for (int j = tid; j < BN; j += kEpiThreads) {
+          const bool ok = n0 + j < a.N;
+          if (a.bias) bias_s[j] = ok ? __half2float(a.bias[n0 + j]) : 0.f;
+          if (EP == 1) {
+            bias_s[BN + j] = ok ? a.bn_mean[n0 + j] : 0.f;
+            bias_s[2 * BN + j] = ok ? a.bn_istd[n0 + j] : 0.f;
+            bias_s[3 * BN + j] = ok && a.bn_gamma ? a.bn_gamma[n0 + j] : 0.f;
+            bias_s[4 * BN + j] = ok && a.bn_beta ? a.bn_beta[n0 + j] : 0.f;
+          }
+        }
         named_sync(2, kEpiThreads);
       }
-      mbar_wait(&tfull[ab], (t >> 1) & 1);
-      tc_fence_after();
       const int row = wq * 32 + lane;
       const int m = m0 + row;
       int ex0 = 0, ey0 = 0, en0 = 0;
@@ -674,6 +692,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int y = tt % a.rgh, n = tt / a.rgh;
         orow = ((int64_t)n * g.h + y * a.rsh + a.ra) * g.w + x * a.rsw + a.rb;
       }
+      mbar_wait(&tfull[ab], (t >> 1) & 1);
+      tc_fence_after();
       int bad = 0;
       if (a.tma_store) {
         // 64-column chunks: round into a 128B-swizzled 32 x 64 staging tile, TMA
@@ -787,6 +807,83 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = __fadd_rn(f[j], bias_s[c + j]);
         }
+        if (EP == 1) {
+          // fused BN backward: transpose the f32 chunk through this warp's
+          // staging buffer (XOR-swizzled, conflict-free both ways), then lane =
+          // column walks the 32 rows, so prev / x / gate loads and the output
+          // stores are row-contiguous across the warp and the column sums need
+          // no shuffles
+          float* sf = reinterpret_cast<float*>(stg + ew * kStgBufs * 4096);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sf[lane * 32 + (j ^ lane)] = f[j];
+          __syncwarp();
+          const int col = nb + lane;
+          const bool colv = col < a.N;
+          const float mu = bias_s[BN + c + lane], is = bias_s[2 * BN + c + lane];
+          const float ga = bias_s[3 * BN + c + lane], be = bias_s[4 * BN + c + lane];
+          float t1 = 0.f, t2 = 0.f;
+          // all 32 rows' loads in flight at once (16-bit values in 32-bit regs)
+          uint32_t xw[32], zw[32], pw[32];
+          const int rlb = wq * 32;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            int64_t ro;
+            bool rv;
+            if (AM == A_TILE4) {
+              const int rl = rlb + r, bx = rl % a.sbw, t2r = rl / a.sbw;
+              ro = ((int64_t)(en0 + t2r / a.sbh) * a.sgh + ey0 + t2r % a.sbh) * a.sgw + ex0 + bx;
+              rv = mv && colv;
+            } else {
+              ro = m0 + rlb + r;
+              rv = m0 + rlb + r < a.M && colv;
+            }
+            const int64_t o = ro * a.ldc + col;
+            const unsigned short* xp = reinterpret_cast<const unsigned short*>(a.bnx) + o;
+            xw[r] = rv ? (uint32_t)__ldg(xp) : 0u;
+            zw[r] = rv && a.bn_gate
+                        ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(a.bn_gate) + o)
+                        : 0u;
+            pw[r] = rv && a.acc ? (uint32_t)*(reinterpret_cast<const unsigned short*>(a.out) + o)
+                                : 0u;
+          }
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            int64_t ro;
+            bool rv;
+            if (AM == A_TILE4) {
+              const int rl = rlb + r, bx = rl % a.sbw, t2r = rl / a.sbw;
+              ro = ((int64_t)(en0 + t2r / a.sbh) * a.sgh + ey0 + t2r % a.sbh) * a.sgw + ex0 + bx;
+              rv = mv && colv;
+            } else {
+              ro = m0 + rlb + r;
+              rv = m0 + rlb + r < a.M && colv;
+            }
+            const float fv = sf[r * 32 + (lane ^ r)];
+            const float pvf = __half2float(__ushort_as_half((unsigned short)pw[r]));
+            const float g = __half2float(__float2half_rn(__fadd_rn(a.acc ? pvf : 0.f, fv)));
+            const float xh = __fmul_rn(
+                __fsub_rn(__half2float(__ushort_as_half((unsigned short)xw[r])), mu), is);
+            float gate = 1.f;
+            if (a.bn_gate) {
+              gate = __half2float(__ushort_as_half((unsigned short)zw[r])) > 0.f ? 1.f : 0.f;
+            } else if (a.bn_relu) {
+              const float z = __half2float(__float2half_rn(__fadd_rn(__fmul_rn(ga, xh), be)));
+              gate = z > 0.f ? 1.f : 0.f;
+            }
+            const float gy = __fmul_rn(g, gate);
+            if (rv) {
+              t1 += gy;
+              t2 += __fmul_rn(gy, xh);
+              a.bn_out[ro * a.ldc + col] = __float2half_rn(a.bn_canon ? __fadd_rn(0.f, gy) : gy);
+            }
+          }
+          if (a.stats) {
+            red[((wq * BN) + c + lane) * 2 + 0] = t1;
+            red[((wq * BN) + c + lane) * 2 + 1] = t2;
+          }
+          continue;
+        }
         __half* dsth = reinterpret_cast<__half*>(a.out) + orow * a.ldc + nb;
         __align__(16) __half hv[32];
         const bool vec = full_cols && (a.ldc % 8 == 0);
@@ -806,6 +903,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) hv[j] = __float2half_rn(__fadd_rn(0.f, f[j]));
           }
+        }
+        // BN statistics of the rounded outputs, 16 columns at a time: column
+        // sums over the warp's 32 rows (lanes l and l^16 add, then a halving
+        // exchange leaves column c + 16h + (lane & 15) in lane; 31 shuffles)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (!a.stats) break;
+          float s1[16], s2[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int j = 16 * h + k;
+            const float x = (mv && nb + j < a.N) ? __half2float(hv[j]) : 0.f;
+            s1[k] = x;
+            s2[k] = x * x;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            s1[j] += __shfl_xor_sync(0xffffffffu, s1[j], 16);
+            s2[j] += __shfl_xor_sync(0xffffffffu, s2[j], 16);
+          }
+#pragma unroll
+          for (int st = 8; st >= 1; st >>= 1) {
+            const bool up = (lane & st) != 0;
+#pragma unroll
+            for (int j = 0; j < st; ++j) {
+              const float send1 = up ? s1[j] : s1[j + st], keep1 = up ? s1[j + st] : s1[j];
+              const float send2 = up ? s2[j] : s2[j + st], keep2 = up ? s2[j + st] : s2[j];
+              s1[j] = keep1 + __shfl_xor_sync(0xffffffffu, send1, st);
+              s2[j] = keep2 + __shfl_xor_sync(0xffffffffu, send2, st);
+            }
+          }
+          if (lane < 16) {
+            red[((wq * BN) + c + 16 * h + lane) * 2 + 0] = s1[0];
+            red[((wq * BN) + c + 16 * h + lane) * 2 + 1] = s2[0];
+          }
+        }
+        if (mv) {
           if (vec) {
 #pragma unroll
             for (int j = 0; j < 32; j += 8)
@@ -818,30 +952,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) bad |= (nb + j < a.N) && !isfinite(__half2float(hv[j]));
           }
-        }
-        if (a.stats) {
-          // column sums over this warp's 32 rows of the ROUNDED outputs: the
-          // halving exchange leaves column (c + lane) in every lane (31 shuffles)
-          float s1[32], s2[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = (mv && nb + j < a.N) ? __half2float(hv[j]) : 0.f;
-            s1[j] = x;
-            s2[j] = x * x;
-          }
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) {
-            const bool up = (lane & st) != 0;
-#pragma unroll
-            for (int j = 0; j < st; ++j) {
-              const float send1 = up ? s1[j] : s1[j + st], keep1 = up ? s1[j + st] : s1[j];
-              const float send2 = up ? s2[j] : s2[j + st], keep2 = up ? s2[j + st] : s2[j];
-              s1[j] = keep1 + __shfl_xor_sync(0xffffffffu, send1, st);
-              s2[j] = keep2 + __shfl_xor_sync(0xffffffffu, send2, st);
-            }
-          }
-          red[((wq * BN) + c + lane) * 2 + 0] = s1[0];
-          red[((wq * BN) + c + lane) * 2 + 1] = s2[0];
         }
       }
       // the accumulator buffer can be reused by the MMA warp
@@ -1643,7 +1753,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     const bool b_tma = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN || pl.bmode == B_IM2COL ||
                        pl.bmode == B_TILE4;
     const int pol = cta_pair_policy();
-    if (pol && a_tma && b_tma && pl.bn >= 128 && pl.M > BM &&
+    if (pol && a_tma && b_tma && pl.bn >= 128 && pl.M > BM && !pb.bnx &&
         (pol == 2 || (pl.bn == 256 && pl.kb_per_split >= 16)))
       tile_and_split(2);
   }
@@ -1666,10 +1776,10 @@ static int plan_grid(const Plan& pl) {
   return (pl.units < pairs ? pl.units : pairs) * pl.cg;
 }
 
-template <int BN, int AM, int BMD, int CG, int RB = 0>
+template <int BN, int AM, int BMD, int CG, int RB = 0, int EP = 0>
 static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
                      const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
-  auto kern = k_tc_gemm<BN, AM, BMD, CG, RB>;
+  auto kern = k_tc_gemm<BN, AM, BMD, CG, RB, EP>;
   using C = Cfg<BN, CG, RB>;
   static bool attr = false;
   if (!attr) {
@@ -1698,6 +1808,18 @@ static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& t
 template <int BN>
 static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
                        const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
+  if (args.bnx) {  // fused BN-backward statistics: dgrad modes, single-CTA tiles
+#define NNL_TC_BNB(AM, BMD)                                                    \
+    if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1)                       \
+      return pl.resb ? launch_tc<BN, AM, BMD, 1, 1, 1>(pl, ta, tb, tc, args, st)  \
+                     : launch_tc<BN, AM, BMD, 1, 0, 1>(pl, ta, tb, tc, args, st);
+    NNL_TC_BNB(A_TMA_K, B_TMA_MN)
+    NNL_TC_BNB(A_TILE4, B_TMA_MN)
+    NNL_TC_BNB(A_IM2COL, B_TMA_MN)
+#undef NNL_TC_BNB
+    return fail(NNL_ERR_UNSUPPORTED, "no fused BN-backward kernel for mode %d/%d", pl.amode,
+                pl.bmode);
+  }
 #define NNL_TC_CASE(AM, BMD)                                                   \
   if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1 && !pl.resb)             \
     return launch_tc<BN, AM, BMD, 1>(pl, ta, tb, tc, args, st);
@@ -1774,6 +1896,20 @@ int32_t tc_stat_rows(const GemmProblem& pb, int dtype) {
   if (!pl.ok || pb.mode != kFprop || pb.g.affine || pl.N > Cfg<64>::MAX_STAT_N) return 0;
   // one partial row per persistent CTA
   return plan_grid(pl);
+}
+
+int32_t tc_bnb_rows(const GemmProblem& pb, int dtype) {
+  if (dtype != NNL_F16 || pb.mode != kDgrad || pb.g.affine) return 0;
+  GemmProblem q = pb;
+  float dummy;
+  q.stats = &dummy;  // no split-K
+  q.bnx = &dummy;    // single-CTA tiles
+  Plan pl = make_plan(q);
+  if (!pl.ok || pl.remap || pl.nclass || pl.N > Cfg<64>::MAX_STAT_N || pl.N % 8) return 0;
+  const bool mode_ok = (pl.amode == A_TMA_K && pl.bmode == B_TMA_MN) ||
+                       (pl.amode == A_TILE4 && pl.bmode == B_TMA_MN) ||
+                       (pl.amode == A_IM2COL && pl.bmode == B_TMA_MN);
+  return mode_ok ? plan_grid(pl) : 0;
 }
 
 static inline uint8_t* align256(uint8_t* p) {
@@ -1917,6 +2053,15 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   memcpy(args.tap_offh, pl.tap_offh, sizeof(args.tap_offh));
   args.bias = reinterpret_cast<const __half*>(pb.bias);
   args.stats = pb.stats; args.nonfinite = pb.nonfinite;
+  if (pb.bnx) {
+    if (pl.remap || pl.nclass) return fail(NNL_ERR_UNSUPPORTED, "fused BN backward with remap");
+    args.bnx = reinterpret_cast<const __half*>(pb.bnx);
+    args.bn_gate = reinterpret_cast<const __half*>(pb.bn_gate);
+    args.bn_mean = pb.bn_mean; args.bn_istd = pb.bn_istd;
+    args.bn_gamma = pb.bn_gamma; args.bn_beta = pb.bn_beta;
+    args.bn_relu = pb.bn_relu; args.bn_canon = pb.bn_canon;
+    args.bn_out = reinterpret_cast<__half*>(pb.bn_out ? pb.bn_out : pb.out);
+  }
   args.K = pl.K;
   args.sbw = pl.sbw; args.sbh = pl.sbh; args.sbi = pl.sbi; args.stw = pl.stw; args.sth = pl.sth;
   args.sp_tiles = pl.sp_tiles; args.slw = pl.slw; args.slh = pl.slh;
@@ -1930,7 +2075,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   }
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
-  if (!args.partial && !args.acc && !args.remap && use_tma_store() &&
+  if (!args.partial && !args.acc && !args.remap && !args.bnx && use_tma_store() &&
       !(reinterpret_cast<uintptr_t>(pb.out) & 15) && (pl.ldc * 2) % 16 == 0) {
     View o;
     o.ptr = pb.out; o.rows = pl.M; o.cols = pl.N; o.ld = pl.ldc;

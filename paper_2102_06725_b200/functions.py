@@ -214,14 +214,50 @@ class Convolution(FunctionImpl):
         _lib.call("nnl_conv2d_fwd", C.byref(cs), x.code, x.ptr, w.ptr, b.ptr, ys[0].ptr,
                   stats.data_ptr() if stats is not None else None, ws[0], ws[1], _st())
 
+    def bnb_rows(self, node) -> int:
+        """Partial rows of the dgrad with the preceding BN's backward statistics
+        fused into its epilogue (0: not available for this shape)."""
+        x = node.inputs[0].data
+        if x.dtype is not Dtype.F16:
+            return 0
+        cs = self.shape_struct(x.shape)
+        return int(_lib.lib().nnl_conv2d_bwd_data_bn_rows(C.byref(cs), x.code))
+
+    def _dgrad_bn(self, node, cs, x, w, gy, gx, acc0, plan, ws):
+        """dgrad + the statistics pass of the BN before this convolution
+        (engine fusion, graph.py backward): writes the gated gradient to
+        plan["out"] (or gx) and (gy, gy*xhat) column partials to the BN."""
+        bn = plan["bn"]
+        bx = bn.inputs[0].data
+        c = bx.shape[1]
+        rows = plan["rows"]
+        parts = _state_buf(bn, "bwd_parts", rows * 2 * c)
+        gate = plan.get("gate")
+        out = plan.get("out")
+        relu = plan["kind"] == "relu"
+        bf = _lib.BnBwdFuse(bx.ptr, gate.ptr if gate is not None else None,
+                            bn.inputs[1].data.ptr if relu else None,
+                            bn.inputs[2].data.ptr if relu else None,
+                            bn.state["mean"].data_ptr(), bn.state["istd"].data_ptr(),
+                            1 if relu else 0, 0 if relu else 1,
+                            out.ptr if out is not None else None, parts.data_ptr())
+        _lib.call("nnl_conv2d_bwd_data_bn", C.byref(cs), x.code, gy.ptr, w.ptr, gx.ptr,
+                  _flag(acc0), C.byref(bf), ws[0], ws[1], _st())
+        bn.state["bwd_fused"] = {"parts": parts, "rows": rows,
+                                 "gy": out if out is not None else gx}
+
     def backward(self, node, gys, gxs, acc):
         x, w = node.inputs[0].data, node.inputs[1].data
         gy = gys[0]
         cs = self.shape_struct(x.shape)
         if gxs[0] is not None:
             ws = _lib.workspace(_lib.lib().nnl_conv2d_workspace_size(C.byref(cs), x.code, 1))
-            _lib.call("nnl_conv2d_bwd_data", C.byref(cs), x.code, gy.ptr, w.ptr, gxs[0].ptr,
-                      _flag(acc[0]), ws[0], ws[1], _st())
+            plan = node.state.pop("bnb", None)
+            if plan is not None:
+                self._dgrad_bn(node, cs, x, w, gy, gxs[0], acc[0], plan, ws)
+            else:
+                _lib.call("nnl_conv2d_bwd_data", C.byref(cs), x.code, gy.ptr, w.ptr, gxs[0].ptr,
+                          _flag(acc[0]), ws[0], ws[1], _st())
         # the bias gradient was already reduced by the following BN's backward
         gb = None if node.state.get("bias_by_bn") else gxs[2]
         if gxs[1] is not None or gb is not None:
@@ -451,10 +487,35 @@ class BatchNormalization(FunctionImpl):
                   gxs[2].ptr if gxs[2] is not None else None, _flag(acc[2]),
                   cbias, 0, node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
 
+    def _backward_apply(self, node, fz, gxs, acc):
+        """Backward whose statistics pass ran in the next convolution's dgrad
+        epilogue (Convolution._dgrad_bn): finalize + apply only."""
+        x = node.inputs[0].data
+        gamma = node.inputs[1].data
+        c = x.shape[1]
+        rows = self._rows(x)
+        ws = _lib.workspace(_lib.lib().nnl_bn_workspace_size(rows, c))
+        conv = node.inputs[0].parent
+        cbias = None
+        if gxs[0] is not None and conv is not None and conv.state.get("bias_by_bn"):
+            cbias = conv.inputs[2].grad.ptr
+        _lib.call("nnl_bn_bwd_apply", x.code, rows, c, x.ptr, fz["gy"].ptr,
+                  fz["parts"].data_ptr(), fz["rows"], gamma.ptr,
+                  node.state["mean"].data_ptr(), node.state["istd"].data_ptr(),
+                  1 if self.batch_stat else 0,
+                  gxs[0].ptr if gxs[0] is not None else None, _flag(acc[0]),
+                  gxs[1].ptr if gxs[1] is not None else None, _flag(acc[1]),
+                  gxs[2].ptr if gxs[2] is not None else None, _flag(acc[2]),
+                  cbias, 0, node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
+
     def backward(self, node, gys, gxs, acc):
         self._backward(node, gys[0], False, gxs, acc)
 
     def backward_fused(self, node, relu_node, gxs, acc):
+        fz = node.state.pop("bwd_fused", None)
+        if fz is not None:
+            self._backward_apply(node, fz, gxs, acc)
+            return
         self._backward(node, relu_node.outputs[0].grad, True, gxs, acc)
 
     # residual tail BN -> Add2 -> ReLU (engine fusion, graph.py::_plan): the
@@ -464,6 +525,10 @@ class BatchNormalization(FunctionImpl):
         self._forward(node, relu_node.outputs[0].data, relu=True, residual=residual)
 
     def backward_residual(self, node, relu_node, gxs, acc, dres, acc_res):
+        fz = node.state.pop("bwd_fused", None)
+        if fz is not None:  # the gated gradient (= dres) and statistics are done
+            self._backward_apply(node, fz, gxs, acc)
+            return
         z = relu_node.outputs[0]
         self._backward(node, z.grad, False, gxs, acc, gate=z.data, dres=dres, acc_res=acc_res)
 

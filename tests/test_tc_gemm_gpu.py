@@ -310,3 +310,61 @@ def test_spatial_tiles_match_im2col(nnl, geom):
             _lib.lib().nnl_set_tc_tile4(prev)
     for a, c in zip(outs[0], outs[1]):
         assert _rel_err(a, c) < 2e-3
+
+
+@pytest.mark.parametrize("geom,tail", [((4, 64, 128, 1, 1, 0, 16), False),
+                                       ((4, 64, 64, 3, 1, 1, 16), False),
+                                       ((4, 256, 64, 1, 1, 0, 16), True)])
+def test_dgrad_bn_stats_epilogue(nnl, geom, tail):
+    """nnl_conv2d_bwd_data_bn against nnl_conv2d_bwd_data + the BN-backward
+    statistics computed here: identical gated gradient bits, column sums of
+    (gy, gy*xhat) within f32 summation-order noise."""
+    import torch
+    from paper_2102_06725_b200 import _lib
+    b, cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(5)
+    dev = torch.device("cuda")
+    h16 = lambda a: torch.from_numpy(O.q16(a.astype(np.float32))).to(dev).half()
+    dy = h16(rng.uniform(-1, 1, (b, hw, hw, cout)))
+    w = h16(rng.uniform(-0.1, 0.1, (cout, k, k, cin)))
+    x = h16(rng.uniform(-2, 2, (b, hw, hw, cin)))
+    gate = h16(rng.uniform(-1, 1, (b, hw, hw, cin)))
+    prev = h16(rng.uniform(-1, 1, (b, hw, hw, cin)))
+    mean = torch.from_numpy(rng.uniform(-0.2, 0.2, cin).astype(np.float32)).to(dev)
+    istd = torch.from_numpy(rng.uniform(0.5, 1.5, cin).astype(np.float32)).to(dev)
+    gam = torch.from_numpy(rng.uniform(0.5, 1.5, cin).astype(np.float32)).to(dev)
+    bet = torch.from_numpy(rng.uniform(-0.5, 0.5, cin).astype(np.float32)).to(dev)
+    cs = _lib.ConvShape(b, hw, hw, cin, cout, k, k, s, s, p, p, hw, hw)
+    L = _lib.lib()
+    ws_n = L.nnl_conv2d_workspace_size(C.byref(cs), _lib.F16, 1)
+    ws = torch.empty(ws_n, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    ref = prev.clone() if tail else torch.empty_like(x)
+    _lib.call("nnl_conv2d_bwd_data", C.byref(cs), _lib.F16, dy.data_ptr(), w.data_ptr(),
+              ref.data_ptr(), 1 if tail else 0, ws.data_ptr(), ws_n, st)
+    rows = L.nnl_conv2d_bwd_data_bn_rows(C.byref(cs), _lib.F16)
+    assert rows > 0
+    parts = torch.zeros(rows * 2 * cin, dtype=torch.float32, device=dev)
+    dx = prev.clone() if tail else torch.empty_like(x)
+    out = torch.empty_like(x) if tail else None
+    bf = _lib.BnBwdFuse(x.data_ptr(), gate.data_ptr() if tail else None,
+                        None if tail else gam.data_ptr(), None if tail else bet.data_ptr(),
+                        mean.data_ptr(), istd.data_ptr(), 0 if tail else 1, 1 if tail else 0,
+                        out.data_ptr() if tail else None, parts.data_ptr())
+    _lib.call("nnl_conv2d_bwd_data_bn", C.byref(cs), _lib.F16, dy.data_ptr(), w.data_ptr(),
+              dx.data_ptr(), 1 if tail else 0, C.byref(bf), ws.data_ptr(), ws_n, st)
+    torch.cuda.synchronize()
+    g = ref.float().cpu().numpy().reshape(-1, cin)
+    xf = x.float().cpu().numpy().reshape(-1, cin)
+    xh = (xf - mean.cpu().numpy()) * istd.cpu().numpy()
+    if tail:
+        gt = (gate.float().cpu().numpy().reshape(-1, cin) > 0).astype(np.float32)
+    else:
+        z = O.q16(gam.cpu().numpy() * xh + bet.cpu().numpy())
+        gt = (z > 0).astype(np.float32)
+    gy = g * gt
+    got = (out if tail else dx).float().cpu().numpy().reshape(-1, cin)
+    assert np.array_equal(got, O.q16(gy + 0.0 if tail else gy))
+    sums = parts.cpu().numpy().reshape(rows, 2, cin).sum(0)
+    want = np.stack([gy.sum(0, dtype=np.float64), (gy * xh).sum(0, dtype=np.float64)])
+    np.testing.assert_allclose(sums, want, rtol=1e-4, atol=1e-3)

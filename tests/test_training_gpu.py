@@ -375,3 +375,62 @@ def test_overlapped_nccl_allreduce_world1_matches_local(nnl):
             assert np.array_equal(v, runs[1][1][k]), k
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("net", ["bottleneck", "basic"])
+def test_bn_backward_stats_in_dgrad_epilogue(nnl, net):
+    """BN-backward statistics fused into the dgrad epilogue of the following
+    convolution (fused BN->ReLU->conv, and the residual tail's last gradient
+    contributor writing the gated gradient straight into the shortcut's
+    gradient) against the same engine with that fusion off: the same step up
+    to the f32 summation order of the statistics.  (The kernel itself is
+    checked bit for bit in test_dgrad_bn_stats_epilogue.)"""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import graph, networks
+    _ctx(nnl, True)
+    prev_flag = graph.BNB_FUSION
+    B, hw = 8, 16
+    x = O.uniform(3, 0, (B, 64, hw, hw), 0, 1)
+    lab = (np.arange(B) % 10).astype(np.float32)
+    block = networks._bottleneck if net == "bottleneck" else networks._basic
+    runs, fused = [], []
+    try:
+        for bnb in (True, False):
+            graph.BNB_FUSION = bnb
+            with nnl.registry_scope(nnl.ParameterRegistry(0)) as reg:
+                xv = nnl.Variable(x.shape, need_grad=True)
+                tv = nnl.Variable(lab.shape)
+                h = xv
+                blocks = [(64, 1, True), (64, 1, False), (64, 2, True), (64, 1, False)]
+                for i, (w, s, proj) in enumerate(blocks):
+                    with nnl.parameter_scope(f"b{i}"):
+                        h = block(h, w, s, proj)
+                h = F.global_average_pooling(h)
+                loss = F.softmax_cross_entropy(nnl.parametric.affine(h, 10, name="fc"), tv)
+                xv.d = x
+                tv.d = lab
+                loss.forward(clear_buffer=True)
+                loss.backward(grad_seed=8.0, clear_buffer=True)
+                grads = {k: v.g for k, v in reg.get_parameters().items()}
+                grads["x"] = xv.g
+                fused.append(sum(1 for n in _nodes(loss) if n.kind == "BatchNormalization"
+                                 and "bwd_parts" in n.state))
+                runs.append((float(loss.d), grads))
+    finally:
+        graph.BNB_FUSION = prev_flag
+    # bottleneck: 3 stride-1 conv2 dgrads (BN1), 4 conv3 dgrads (BN2), 3 tails;
+    # basic: 4 conv2 dgrads (BN1), 2 tails (stride-1 conv1 of the next block)
+    assert fused == [10 if net == "bottleneck" else 6, 0]
+    assert runs[0][0] == runs[1][0]
+    # conv biases feeding a train-mode BN have a mathematically zero gradient
+    # (rounding noise on both sides): floor relative to the largest norm
+    norms = [np.linalg.norm(v) for v in runs[1][1].values()]
+    for k, a in runs[0][1].items():
+        b = runs[1][1][k]
+        den = max(np.linalg.norm(b), 1e-2 * max(norms))
+        assert np.linalg.norm(a - b) / den < 2e-2, k
+
+
+def _nodes(loss):
+    from paper_2102_06725_b200.graph import _ancestors
+    return _ancestors(loss)
