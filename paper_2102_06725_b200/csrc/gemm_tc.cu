@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint64_t* bfull = reinterpret_cast<uint64_t*>(misc + 512);  // RB: resident B landed
+  // accumulate-mode epilogue: per epilogue warp, two prev-tile TMA loads in flight
+  uint64_t* ebar = reinterpret_cast<uint64_t*>(misc + 256);  // [8 warps][2 buffers]
   float* red = reinterpret_cast<float*>(misc + 1024);
   float* bias_s = reinterpret_cast<float*>(misc + 1024 + C::RED_BYTES);
   float* stat_s = reinterpret_cast<float*>(misc + 1024 + C::RED_BYTES + C::BIAS_BYTES);
@@ -245,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[b], kEpi * CG);
     }
     mbar_init(bfull, 1);
+    for (int b = 0; b < 16; ++b) mbar_init(&ebar[b], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -657,6 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     int t = 0;
     uint32_t sb = 0;  // TMA-store staging buffer alternation (per warp)
+    uint32_t ac = 0;  // accumulate mode: chunks processed by this warp (2 KB buffers)
     // the leader's tempty barriers (the MMA waits on both CTAs' epilogues)
     const uint32_t te0 = CG == 2 ? mapa_shared(&tempty[0], 0) : smem_u32(&tempty[0]);
     for (int u = pair; u < a.units; u += npairs, ++t) {
@@ -692,10 +696,78 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int y = tt % a.rgh, n = tt / a.rgh;
         orow = ((int64_t)n * g.h + y * a.rsh + a.ra) * g.w + x * a.rsw + a.rb;
       }
+      // accumulate mode through TMA: the previous values of each 32-column chunk
+      // are TMA-loaded into the staging buffer (two 2 KB halves per warp,
+      // alternating), updated in place to q(prev + acc) and TMA-stored; chunk
+      // 0's load is issued before the accumulator is ready, chunk i+1's while
+      // chunk i is processed
+      const bool tacc = a.tma_store && a.acc;
+      auto acc_load = [&](int cc, uint32_t k) {
+        if (lane == 0) {
+          uint8_t* bb = stg + ew * kStgBufs * 4096 + (k & 1) * 2048;
+          bulk_wait_read<0>();  // this half's previous store has read it
+          mbar_arrive_tx(&ebar[ew * 2 + (k & 1)], 2048);
+          if (AM == A_TILE4) {
+            const int rr = 32 * wq, t2 = rr / a.sbw;
+            tma_load_4d(bb, &tmC, &ebar[ew * 2 + (k & 1)], n0 + cc, ex0 + rr % a.sbw,
+                        ey0 + t2 % a.sbh, en0 + t2 / a.sbh);
+          } else {
+            tma_load_2d(bb, &tmC, &ebar[ew * 2 + (k & 1)], n0 + cc, m0 + 32 * wq);
+          }
+        }
+      };
+      if (tacc) acc_load(c_lo, ac);
       mbar_wait(&tfull[ab], (t >> 1) & 1);
       tc_fence_after();
       int bad = 0;
-      if (a.tma_store) {
+      if (tacc) {
+        for (int c = c_lo; c < c_hi; c += 32, ++ac) {
+          if (c + 32 < c_hi) acc_load(c + 32, ac + 1);
+          uint32_t v[32];
+          tmem_ld32_nowait(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
+          tmem_wait_ld();
+          uint8_t* buf = stg + ew * kStgBufs * 4096 + (ac & 1) * 2048;
+          mbar_wait(&ebar[ew * 2 + (ac & 1)], (ac >> 1) & 1);
+          const int swz = (lane >> 1) & 3;  // 64 B rows, 64 B swizzle
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4* pp = reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ swz) << 4));
+            const uint4 pv = *pp;
+            const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = 8 * j + 2 * e;
+              float f0 = __uint_as_float(v[k]), f1 = __uint_as_float(v[k + 1]);
+              if (a.bias) {
+                f0 = __fadd_rn(f0, bias_s[c + k]);
+                f1 = __fadd_rn(f1, bias_s[c + k + 1]);
+              }
+              const float2 p2 = __half22float2(*reinterpret_cast<const __half2*>(&pw[e]));
+              const __half2 h = __floats2half2_rn(__fadd_rn(p2.x, f0), __fadd_rn(p2.y, f1));
+              pk[e] = mv ? *reinterpret_cast<const uint32_t*>(&h) : 0u;
+            }
+            if (a.nonfinite) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                bad |= ((pk[e] & 0x7c00u) == 0x7c00u) | ((pk[e] & 0x7c000000u) == 0x7c000000u);
+            }
+            *pp = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            if (AM == A_TILE4) {
+              const int rr = 32 * wq, t2 = rr / a.sbw;
+              tma_store_4d(&tmC, buf, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
+                           en0 + t2 / a.sbh);
+            } else {
+              tma_store_2d(&tmC, buf, n0 + c, m0 + 32 * wq);
+            }
+            bulk_commit();
+          }
+        }
+      } else if (a.tma_store) {
         // 64-column chunks: round into a 128B-swizzled 32 x 64 staging tile, TMA
         // store it (rows >= M and columns >= N are clipped by the tensor map),
         // and take the BN column sums from the staged (rounded) values.
@@ -1391,6 +1463,15 @@ struct Plan {
 };
 
 static bool use_tile4() { return nnl_set_tc_tile4(-1) >= 1; }
+// accumulate-mode outputs through TMA load/store (env NNL_TMA_ACC=0: direct stores)
+static bool use_tma_acc_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NNL_TMA_ACC");
+    v = e && e[0] == '0' ? 0 : 1;
+  }
+  return v == 1;
+}
 
 static int pow2_div(int v, int cap) {
   int p = 1;
@@ -2075,7 +2156,8 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   }
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
-  if (!args.partial && !args.acc && !args.remap && !args.bnx && use_tma_store() &&
+  if (!args.partial && !args.remap && !args.bnx && !(args.acc && args.stats) &&
+      (!args.acc || use_tma_acc_env()) && use_tma_store() &&
       !(reinterpret_cast<uintptr_t>(pb.out) & 15) && (pl.ldc * 2) % 16 == 0) {
     View o;
     o.ptr = pb.out; o.rows = pl.M; o.cols = pl.N; o.ld = pl.ldc;
@@ -2083,7 +2165,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const bool gather = pl.amode == A_GATHER_FPROP || pl.amode == A_GATHER_DGRAD ||
                         pl.amode == A_GATHER_C4 || pl.bmode == B_GATHER_WGRAD ||
                         pl.bmode == B_GATHER_C4;
-    const bool cw32 = !gather && pl.bn == 64;
+    const bool cw32 = (!gather && pl.bn == 64) || args.acc;  // acc: 32-column chunks
     const CUtensorMapSwizzle sw = cw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
     if (pl.amode == A_TILE4) {  // 32-row sub-boxes of the pixel box over the output grid
       const int bw32 = pl.sbw < 32 ? pl.sbw : 32;
