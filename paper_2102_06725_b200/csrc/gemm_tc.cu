@@ -64,7 +64,9 @@ constexpr int BM = 128, BK = 64, kThreads = 384;
 // streams A only (weight-stationary narrow convolutions).
 constexpr int RES_MAX = 96 * 1024;
 
-template <int BN, int CG = 1, int RB = 0>
+// EP = 1 (fused BN-backward epilogue): each of the 8 epilogue warps keeps two
+// 6 KB sets of TMA-loaded input tiles (x, gate, prev: 32 rows x 32 columns each)
+template <int BN, int CG = 1, int RB = 0, int EP = 0>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // this CTA's share of B
@@ -76,7 +78,7 @@ struct Cfg {
   static constexpr int MAX_STAT_N = 2048;  // per-CTA BN statistics accumulator [2][N]
   static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
   // TMA-store staging: 8 x 4 KB (4 warps x 2 buffers, or 8 warps x 1)
-  static constexpr int STG_BYTES = 4 * 2 * 4096;
+  static constexpr int STG_BYTES = EP ? 8 * 2 * 6144 : 4 * 2 * 4096;
   static constexpr int FIXED =
       1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + STG_BYTES + 1024 + RES_BYTES;
   static constexpr int BUDGET = 232448;
@@ -85,6 +87,12 @@ struct Cfg {
   static constexpr int PIPE = STAGES * (A_BYTES + STAGE_B);
   static constexpr int SMEM = PIPE + FIXED;
   static_assert(STAGES >= 3, "pipeline too shallow");
+};
+
+// tensor maps of the fused BN-backward epilogue (EP = 1): the BN input x, the
+// residual gate and the gated-gradient destination, 32 x 32 boxes, 64 B swizzle
+struct EpiMaps {
+  CUtensorMap x, g, o;
 };
 
 struct TcArgs {
@@ -188,8 +196,9 @@ __device__ __forceinline__ void c4_chunk(uint8_t* dst, const TcArgs& a, const Co
 template <int BN, int AM, int BMD, int CG, int RB, int EP>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmC, const TcArgs a) {
-  using C = Cfg<BN, CG, RB>;
+              const __grid_constant__ CUtensorMap tmC, const __grid_constant__ EpiMaps em,
+              const TcArgs a) {
+  using C = Cfg<BN, CG, RB, EP>;
   constexpr int S = C::STAGES;
   constexpr int BNL = BN / CG;  // B columns held by this CTA
   constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD || AM == A_GATHER_C4;
@@ -716,11 +725,122 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       };
-      if (tacc) acc_load(c_lo, ac);
+      // EP = 1: the x / gate / prev tiles of each 32-column chunk, TMA-loaded into
+      // one of this warp's two 6 KB sets (next chunk prefetched, first chunk before
+      // the accumulator is ready)
+      auto bnb_load = [&](int cc, uint32_t k) {
+        if (lane == 0) {
+          uint8_t* bb = stg + ew * 12288 + (k & 1) * 6144;
+          uint64_t* bar = &ebar[ew * 2 + (k & 1)];
+          bulk_wait_read<0>();  // this set's previous store has read it
+          mbar_arrive_tx(bar, 2048u * (1u + (a.bn_gate ? 1u : 0u) + (a.acc ? 1u : 0u)));
+          if (AM == A_TILE4) {
+            const int rr = 32 * wq, t2 = rr / a.sbw;
+            const int cx = ex0 + rr % a.sbw, cy = ey0 + t2 % a.sbh, cn = en0 + t2 / a.sbh;
+            tma_load_4d(bb, &em.x, bar, n0 + cc, cx, cy, cn);
+            if (a.bn_gate) tma_load_4d(bb + 2048, &em.g, bar, n0 + cc, cx, cy, cn);
+            if (a.acc) tma_load_4d(bb + 4096, &tmC, bar, n0 + cc, cx, cy, cn);
+          } else {
+            tma_load_2d(bb, &em.x, bar, n0 + cc, m0 + 32 * wq);
+            if (a.bn_gate) tma_load_2d(bb + 2048, &em.g, bar, n0 + cc, m0 + 32 * wq);
+            if (a.acc) tma_load_2d(bb + 4096, &tmC, bar, n0 + cc, m0 + 32 * wq);
+          }
+        }
+      };
+      if (EP == 1) bnb_load(c_lo, ac);
+      else if (tacc) acc_load(c_lo, ac);
       mbar_wait(&tfull[ab], (t >> 1) & 1);
       tc_fence_after();
       int bad = 0;
-      if (tacc) {
+      if (EP == 1) {
+        // fused BN backward (TcArgs::bnx): row `lane`, 8 columns per 16 B piece;
+        // g = q(prev + acc), gy = g * gate, out = q(gy) written over the x tile and
+        // TMA-stored; column sums of (gy, gy*xhat) by shuffles, 16 columns at a time
+        for (int c = c_lo; c < c_hi; c += 32, ++ac) {
+          if (c + 32 < c_hi) bnb_load(c + 32, ac + 1);
+          uint32_t v[32];
+          tmem_ld32_nowait(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
+          tmem_wait_ld();
+          uint8_t* bs = stg + ew * 12288 + (ac & 1) * 6144;
+          mbar_wait(&ebar[ew * 2 + (ac & 1)], (ac >> 1) & 1);
+          const int swz = (lane >> 1) & 3;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float s1[16], s2[16];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const int j = 2 * h + jj;
+              const int off = lane * 64 + ((j ^ swz) << 4);
+              const uint4 xq = *reinterpret_cast<const uint4*>(bs + off);
+              const uint4 gq = a.bn_gate ? *reinterpret_cast<const uint4*>(bs + 2048 + off)
+                                         : make_uint4(0, 0, 0, 0);
+              const uint4 pq = a.acc ? *reinterpret_cast<const uint4*>(bs + 4096 + off)
+                                     : make_uint4(0, 0, 0, 0);
+              const __half* xh8 = reinterpret_cast<const __half*>(&xq);
+              const __half* gh8 = reinterpret_cast<const __half*>(&gq);
+              const __half* ph8 = reinterpret_cast<const __half*>(&pq);
+              __align__(16) __half o8[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int k = 8 * j + e;
+                const float f = __uint_as_float(v[k]);
+                const float g = __half2float(__float2half_rn(
+                    __fadd_rn(a.acc ? __half2float(ph8[e]) : 0.f, f)));
+                const float xh = __fmul_rn(__fsub_rn(__half2float(xh8[e]), bias_s[BN + c + k]),
+                                           bias_s[2 * BN + c + k]);
+                float gate = 1.f;
+                if (a.bn_gate) {
+                  gate = __half2float(gh8[e]) > 0.f ? 1.f : 0.f;
+                } else if (a.bn_relu) {
+                  const float z = __half2float(__float2half_rn(
+                      __fadd_rn(__fmul_rn(bias_s[3 * BN + c + k], xh), bias_s[4 * BN + c + k])));
+                  gate = z > 0.f ? 1.f : 0.f;
+                }
+                const float gy = __fmul_rn(g, gate);
+                const bool ok = mv && n0 + c + k < a.N;
+                s1[8 * jj + e] = ok ? gy : 0.f;
+                s2[8 * jj + e] = ok ? __fmul_rn(gy, xh) : 0.f;
+                o8[e] = __float2half_rn(a.bn_canon ? __fadd_rn(0.f, gy) : gy);
+              }
+              *reinterpret_cast<uint4*>(bs + off) = *reinterpret_cast<const uint4*>(o8);
+            }
+            if (a.stats) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                s1[q] += __shfl_xor_sync(0xffffffffu, s1[q], 16);
+                s2[q] += __shfl_xor_sync(0xffffffffu, s2[q], 16);
+              }
+#pragma unroll
+              for (int st = 8; st >= 1; st >>= 1) {
+                const bool up = (lane & st) != 0;
+#pragma unroll
+                for (int q = 0; q < st; ++q) {
+                  const float send1 = up ? s1[q] : s1[q + st], keep1 = up ? s1[q + st] : s1[q];
+                  const float send2 = up ? s2[q] : s2[q + st], keep2 = up ? s2[q + st] : s2[q];
+                  s1[q] = keep1 + __shfl_xor_sync(0xffffffffu, send1, st);
+                  s2[q] = keep2 + __shfl_xor_sync(0xffffffffu, send2, st);
+                }
+              }
+              if (lane < 16) {
+                red[((wq * BN) + c + 16 * h + lane) * 2 + 0] = s1[0];
+                red[((wq * BN) + c + 16 * h + lane) * 2 + 1] = s2[0];
+              }
+            }
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            if (AM == A_TILE4) {
+              const int rr = 32 * wq, t2 = rr / a.sbw;
+              tma_store_4d(&em.o, bs, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
+                           en0 + t2 / a.sbh);
+            } else {
+              tma_store_2d(&em.o, bs, n0 + c, m0 + 32 * wq);
+            }
+            bulk_commit();
+          }
+        }
+      } else if (tacc) {
         for (int c = c_lo; c < c_hi; c += 32, ++ac) {
           if (c + 32 < c_hi) acc_load(c + 32, ac + 1);
           uint32_t v[32];
@@ -879,83 +999,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = __fadd_rn(f[j], bias_s[c + j]);
         }
-        if (EP == 1) {
-          // fused BN backward: transpose the f32 chunk through this warp's
-          // staging buffer (XOR-swizzled, conflict-free both ways), then lane =
-          // column walks the 32 rows, so prev / x / gate loads and the output
-          // stores are row-contiguous across the warp and the column sums need
-          // no shuffles
-          float* sf = reinterpret_cast<float*>(stg + ew * kStgBufs * 4096);
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sf[lane * 32 + (j ^ lane)] = f[j];
-          __syncwarp();
-          const int col = nb + lane;
-          const bool colv = col < a.N;
-          const float mu = bias_s[BN + c + lane], is = bias_s[2 * BN + c + lane];
-          const float ga = bias_s[3 * BN + c + lane], be = bias_s[4 * BN + c + lane];
-          float t1 = 0.f, t2 = 0.f;
-          // all 32 rows' loads in flight at once (16-bit values in 32-bit regs)
-          uint32_t xw[32], zw[32], pw[32];
-          const int rlb = wq * 32;
-#pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            int64_t ro;
-            bool rv;
-            if (AM == A_TILE4) {
-              const int rl = rlb + r, bx = rl % a.sbw, t2r = rl / a.sbw;
-              ro = ((int64_t)(en0 + t2r / a.sbh) * a.sgh + ey0 + t2r % a.sbh) * a.sgw + ex0 + bx;
-              rv = mv && colv;
-            } else {
-              ro = m0 + rlb + r;
-              rv = m0 + rlb + r < a.M && colv;
-            }
-            const int64_t o = ro * a.ldc + col;
-            const unsigned short* xp = reinterpret_cast<const unsigned short*>(a.bnx) + o;
-            xw[r] = rv ? (uint32_t)__ldg(xp) : 0u;
-            zw[r] = rv && a.bn_gate
-                        ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(a.bn_gate) + o)
-                        : 0u;
-            pw[r] = rv && a.acc ? (uint32_t)*(reinterpret_cast<const unsigned short*>(a.out) + o)
-                                : 0u;
-          }
-#pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            int64_t ro;
-            bool rv;
-            if (AM == A_TILE4) {
-              const int rl = rlb + r, bx = rl % a.sbw, t2r = rl / a.sbw;
-              ro = ((int64_t)(en0 + t2r / a.sbh) * a.sgh + ey0 + t2r % a.sbh) * a.sgw + ex0 + bx;
-              rv = mv && colv;
-            } else {
-              ro = m0 + rlb + r;
-              rv = m0 + rlb + r < a.M && colv;
-            }
-            const float fv = sf[r * 32 + (lane ^ r)];
-            const float pvf = __half2float(__ushort_as_half((unsigned short)pw[r]));
-            const float g = __half2float(__float2half_rn(__fadd_rn(a.acc ? pvf : 0.f, fv)));
-            const float xh = __fmul_rn(
-                __fsub_rn(__half2float(__ushort_as_half((unsigned short)xw[r])), mu), is);
-            float gate = 1.f;
-            if (a.bn_gate) {
-              gate = __half2float(__ushort_as_half((unsigned short)zw[r])) > 0.f ? 1.f : 0.f;
-            } else if (a.bn_relu) {
-              const float z = __half2float(__float2half_rn(__fadd_rn(__fmul_rn(ga, xh), be)));
-              gate = z > 0.f ? 1.f : 0.f;
-            }
-            const float gy = __fmul_rn(g, gate);
-            if (rv) {
-              t1 += gy;
-              t2 += __fmul_rn(gy, xh);
-              a.bn_out[ro * a.ldc + col] = __float2half_rn(a.bn_canon ? __fadd_rn(0.f, gy) : gy);
-            }
-          }
-          if (a.stats) {
-            red[((wq * BN) + c + lane) * 2 + 0] = t1;
-            red[((wq * BN) + c + lane) * 2 + 1] = t2;
-          }
-          continue;
-        }
         __half* dsth = reinterpret_cast<__half*>(a.out) + orow * a.ldc + nb;
         __align__(16) __half hv[32];
         const bool vec = full_cols && (a.ldc % 8 == 0);
@@ -1057,7 +1100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.stats[((int64_t)blockIdx.x * 2 + 1) * a.N + col] = stat_s[C::MAX_STAT_N + col];
       }
     }
-    if (a.tma_store && lane == 0) bulk_wait<0>();
+    if ((a.tma_store || EP == 1) && lane == 0) bulk_wait<0>();
   }
   __syncwarp();
   tc_fence_before();
@@ -1790,6 +1833,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   }
   if (pl.bmode == B_TMA_MN && pl.b_kblk == 0) pl.b_kblk = 1 << 30;
   pl.bn = pick_bn(pl, pl.bmode == B_TMA_MN && pl.b_tap_stride && !k1);
+  if (pb.bnx && pl.bn > 128) pl.bn = 128;  // the fused BN-backward epilogue's smem budget
   if (pl.remap && pl.N % pl.bn) pl.bn = 64;
   pl.num_kb = (int)cdiv(pl.K, BK);
   auto tile_and_split = [&](int cg) {
@@ -1843,7 +1887,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     const bool b_ok = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN;
     const bool a_ok = pl.amode == A_TMA_K || pl.amode == A_IM2COL || pl.amode == A_IM2COL16 ||
                       pl.amode == A_TILE4;
-    pl.resb = use_resident_b() && b_ok && a_ok && pl.cg == 1 && pl.tiles_n == 1 &&
+    pl.resb = use_resident_b() && b_ok && a_ok && pl.cg == 1 && pl.tiles_n == 1 && !pb.bnx &&
             pl.splits == 1 && (int64_t)pl.num_kb * pl.bn * BK * 2 <= RES_MAX;
   }
   if (pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad))
@@ -1859,9 +1903,10 @@ static int plan_grid(const Plan& pl) {
 
 template <int BN, int AM, int BMD, int CG, int RB = 0, int EP = 0>
 static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
-                     const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
+                     const CUtensorMap& tc, const EpiMaps& em, const TcArgs& args,
+                     cudaStream_t st) {
   auto kern = k_tc_gemm<BN, AM, BMD, CG, RB, EP>;
-  using C = Cfg<BN, CG, RB>;
+  using C = Cfg<BN, CG, RB, EP>;
   static bool attr = false;
   if (!attr) {
     NNL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1881,35 +1926,37 @@ static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& t
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
-  NNL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, args));
+  NNL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, em, args));
   count_launch();
   return NNL_OK;
 }
 
 template <int BN>
 static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
-                       const CUtensorMap& tc, const TcArgs& args, cudaStream_t st) {
-  if (args.bnx) {  // fused BN-backward statistics: dgrad modes, single-CTA tiles
+                       const CUtensorMap& tc, const EpiMaps& em, const TcArgs& args,
+                       cudaStream_t st) {
+  if (args.bnx) {  // fused BN-backward statistics: dgrad modes, single-CTA tiles <= 128 wide
 #define NNL_TC_BNB(AM, BMD)                                                    \
-    if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1)                       \
-      return pl.resb ? launch_tc<BN, AM, BMD, 1, 1, 1>(pl, ta, tb, tc, args, st)  \
-                     : launch_tc<BN, AM, BMD, 1, 0, 1>(pl, ta, tb, tc, args, st);
-    NNL_TC_BNB(A_TMA_K, B_TMA_MN)
-    NNL_TC_BNB(A_TILE4, B_TMA_MN)
-    NNL_TC_BNB(A_IM2COL, B_TMA_MN)
+    if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1 && !pl.resb)           \
+      return launch_tc<BN, AM, BMD, 1, 0, 1>(pl, ta, tb, tc, em, args, st);
+    if constexpr (BN <= 128) {
+      NNL_TC_BNB(A_TMA_K, B_TMA_MN)
+      NNL_TC_BNB(A_TILE4, B_TMA_MN)
+      NNL_TC_BNB(A_IM2COL, B_TMA_MN)
+    }
 #undef NNL_TC_BNB
     return fail(NNL_ERR_UNSUPPORTED, "no fused BN-backward kernel for mode %d/%d", pl.amode,
                 pl.bmode);
   }
 #define NNL_TC_CASE(AM, BMD)                                                   \
   if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1 && !pl.resb)             \
-    return launch_tc<BN, AM, BMD, 1>(pl, ta, tb, tc, args, st);
+    return launch_tc<BN, AM, BMD, 1>(pl, ta, tb, tc, em, args, st);
 #define NNL_TC_CASE_RB(AM, BMD)                                                \
   if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1 && pl.resb)              \
-    return launch_tc<BN, AM, BMD, 1, 1>(pl, ta, tb, tc, args, st);
+    return launch_tc<BN, AM, BMD, 1, 1>(pl, ta, tb, tc, em, args, st);
 #define NNL_TC_CASE2(AM, BMD)                                                  \
   if (pl.amode == AM && pl.bmode == BMD && pl.cg == 2)                         \
-    return launch_tc<BN, AM, BMD, 2>(pl, ta, tb, tc, args, st);
+    return launch_tc<BN, AM, BMD, 2>(pl, ta, tb, tc, em, args, st);
   NNL_TC_CASE(A_TMA_K, B_TMA_K)
   NNL_TC_CASE(A_TMA_K, B_TMA_MN)
   NNL_TC_CASE(A_TMA_MN, B_TMA_MN)
@@ -2156,6 +2203,8 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   }
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
+  EpiMaps em;
+  memset(&em, 0, sizeof(em));
   if (!args.partial && !args.remap && !args.bnx && !(args.acc && args.stats) &&
       (!args.acc || use_tma_acc_env()) && use_tma_store() &&
       !(reinterpret_cast<uintptr_t>(pb.out) & 15) && (pl.ldc * 2) % 16 == 0) {
@@ -2177,9 +2226,28 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     }
     args.tma_store = 1;
   }
-  if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, tc, args, st);
-  else if (pl.bn == 128) rc = dispatch_bn<128>(pl, ta, tb, tc, args, st);
-  else rc = dispatch_bn<256>(pl, ta, tb, tc, args, st);
+  if (pb.bnx) {  // x / gate / prev / gated-output maps: 32 x 32 boxes, 64 B swizzle
+    if ((pl.ldc * 2) % 16) return fail(NNL_ERR_UNSUPPORTED, "fused BN-backward: row stride");
+    auto map = [&](CUtensorMap* m, const void* ptr) -> int {
+      if (pl.amode == A_TILE4) {
+        const int bw32 = pl.sbw < 32 ? pl.sbw : 32;
+        const int bh32 = pl.sbh < 32 / bw32 ? pl.sbh : 32 / bw32;
+        const int box[4] = {32, bw32, bh32, 32 / (bw32 * bh32)};
+        return make_tmap4(m, ptr, pl.N, pl.sgw, pl.sgh, pl.sp_n, box, CU_TENSOR_MAP_SWIZZLE_64B);
+      }
+      View v;
+      v.ptr = ptr; v.rows = pl.M; v.cols = pl.N; v.ld = pl.ldc;
+      return make_tmap(m, v, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    };
+    if ((rc = map(&em.x, pb.bnx))) return rc;
+    if (pb.bn_gate && (rc = map(&em.g, pb.bn_gate))) return rc;
+    if ((rc = map(&em.o, pb.bn_out ? pb.bn_out : pb.out))) return rc;
+    if (pb.acc && (rc = map(&tc, pb.out))) return rc;
+    args.tma_store = 0;
+  }
+  if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, tc, em, args, st);
+  else if (pl.bn == 128) rc = dispatch_bn<128>(pl, ta, tb, tc, em, args, st);
+  else rc = dispatch_bn<256>(pl, ta, tb, tc, em, args, st);
   if (rc) return rc;
   if (to_partial) {
     const bool mapped = (pl.c4 || pl.s2d) && pb.mode == kWgrad;
