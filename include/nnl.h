@@ -68,6 +68,10 @@ int nnl_set_tc_s2d4(int enabled);
    filter tap) instead of TMA im2col rows: 0 off, 1 fprop + dgrad (default),
    2 also wgrad; returns the previous setting, < 0 only queries (env NNL_TILE4) */
 int nnl_set_tc_tile4(int enabled);
+/* 3x3 stride-1 convolutions over 64 channels from one shared input halo per
+   (8 x 16)-pixel tile (nine descriptor views) instead of one load per tap;
+   returns the previous setting, < 0 only queries (default 1; env NNL_HALO=0) */
+int nnl_set_tc_halo(int enabled);
 
 /* ---- geometry ----------------------------------------------------------- */
 typedef struct nnl_conv_shape {

@@ -46,8 +46,13 @@ using namespace tc;
 // whose grid the box tiles exactly).
 enum AMode {
   A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4,
-  A_GATHER_C4 = 5, A_IM2COL16 = 6, A_TILE4 = 7, A_TILE4MN = 8
+  A_GATHER_C4 = 5, A_IM2COL16 = 6, A_TILE4 = 7, A_TILE4MN = 8, A_HALO = 9
 };
+// A_HALO: 3x3 stride-1 pad-1 convolutions over 64 channels (one channel block):
+// the (8 x 16)-pixel M tile's input halo (10 x 18 pixels, rows padded to 16 pixels)
+// is ONE tiled 4D TMA box per tile, and the nine taps are nine descriptor views
+// into it (view (r, s) starts at halo row r*16 + s: SBO 2048 B, no base offset),
+// so each input pixel crosses L2 -> SMEM once per tile instead of once per tap.
 enum BMode {
   B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATHER_C4 = 4, B_IM2COL16 = 5,
   B_TILE4 = 6
@@ -66,16 +71,16 @@ constexpr int RES_MAX = 96 * 1024;
 
 // EP = 1 (fused BN-backward epilogue): each of the 8 epilogue warps keeps two
 // 6 KB sets of TMA-loaded input tiles (x, gate, prev: 32 rows x 32 columns each)
-template <int BN, int CG = 1, int RB = 0, int EP = 0>
+template <int BN, int CG = 1, int RB = 0, int EP = 0, int HL = 0>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int A_BYTES = HL ? 16 * 18 * 128 : BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // this CTA's share of B
   static constexpr int STAGE_B = RB ? 0 : B_BYTES;      // B bytes per ring stage
-  static constexpr int RES_BYTES = RB ? RES_MAX : 0;
+  static constexpr int RES_BYTES = RB ? (HL ? 9 * B_BYTES : RES_MAX) : 0;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int RED_BYTES = 4 * BN * 2 * 4;
   static constexpr int BIAS_BYTES = BN * 4 * 5;  // bias + the fused BN-backward constants
-  static constexpr int MAX_STAT_N = 2048;  // per-CTA BN statistics accumulator [2][N]
+  static constexpr int MAX_STAT_N = HL ? 64 : 2048;  // per-CTA BN statistics [2][N]
   static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
   // TMA-store staging: 8 x 4 KB (4 warps x 2 buffers, or 8 warps x 1)
   static constexpr int STG_BYTES = EP ? 8 * 2 * 6144 : 4 * 2 * 4096;
@@ -86,7 +91,7 @@ struct Cfg {
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int PIPE = STAGES * (A_BYTES + STAGE_B);
   static constexpr int SMEM = PIPE + FIXED;
-  static_assert(STAGES >= 3, "pipeline too shallow");
+  static_assert(STAGES >= 3 || (HL && STAGES >= 2), "pipeline too shallow");
 };
 
 // tensor maps of the fused BN-backward epilogue (EP = 1): the BN input x, the
@@ -131,6 +136,7 @@ struct TcArgs {
   // (r, s) of a box at (x0, y0, n0) reads input (x0 + s + slw, y0 + r + slh, n0);
   // the epilogue's output grid is sgw x sgh (A_TILE4: rows -> pixels, 4D store)
   int sbw, sbh, sbi, stw, sth, sp_tiles, slw, slh, sgw, sgh;
+  int res_kb;         // resident-B k-blocks when they differ from num_kb (A_HALO: 9 taps)
   // fused BatchNormalization backward statistics (dgrad of the convolution
   // after a BN[+ReLU]): g = the rounded dgrad output; gy = g * gate with gate
   // = (bn_gate > 0) (residual tail) or (q(gamma*xhat + beta) > 0) (bn_relu),
@@ -198,7 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ EpiMaps em,
               const TcArgs a) {
-  using C = Cfg<BN, CG, RB, EP>;
+  using C = Cfg<BN, CG, RB, EP, AM == A_HALO>;
+  constexpr bool kSp = AM == A_TILE4 || AM == A_HALO;  // spatial pixel-box M tiles
   constexpr int S = C::STAGES;
   constexpr int BNL = BN / CG;  // B columns held by this CTA
   constexpr bool kGA = AM == A_GATHER_FPROP || AM == A_GATHER_DGRAD || AM == A_GATHER_C4;
@@ -275,8 +282,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kTmaBytes && lane == 0) {
       int it = 0;
       if (RB) {  // the whole B operand once (single N tile, no split)
-        mbar_arrive_tx(bfull, (uint32_t)(a.num_kb * C::B_BYTES));
-        for (int kb = 0; kb < a.num_kb; ++kb) {
+        const int rkb = a.res_kb ? a.res_kb : a.num_kb;
+        mbar_arrive_tx(bfull, (uint32_t)(rkb * C::B_BYTES));
+        for (int kb = 0; kb < rkb; ++kb) {
           uint8_t* dst = resB + kb * C::B_BYTES;
           if (BMD == B_TMA_K) {
             tma_load_2d(dst, &tmB, bfull, kb * BK, 0);
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN + rank * BNL;
         // im2col A: window base of the tile's first row pixel
         int a_x = 0, a_y = 0, a_n = 0;
-        if (AM == A_TILE4) sp_origin(a, m0 / BM, a_x, a_y, a_n);
+        if (kSp) sp_origin(a, m0 / BM, a_x, a_y, a_n);
         if (AM == A_IM2COL || AM == A_IM2COL16) {
           a_x = m0 % a.gw;
           const int t = m0 / a.gw;
@@ -348,6 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               loadi2c(stA + s * C::A_BYTES + j * 4096, &tmA, 0, a_x, a_y, a_n, (uint16_t)sx,
                       (uint16_t)r);
             }
+          } else if (AM == A_HALO) {
+            load4d(stA + s * C::A_BYTES, &tmA, 0, a_x + a.slw, a_y + a.slh, a_n);
           } else if (AM == A_TILE4) {
             const int t = kb / a.cblk, cb = kb - t * a.cblk;
             const int r = t / g.s, sx = t - r * g.s;
@@ -452,7 +462,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t db0 = BMD == B_IM2COL16 ? sdesc_sw32(bbase, 2048, 256)
                                : kBmn ? sdesc_sw128(bbase, 8192, 1024)
                                       : sdesc_sw128(bbase, 16, 1024);
-          if (elect_one()) {
+          if (AM == A_HALO) {
+            if (elect_one()) {
+              for (int tp = 0; tp < 9; ++tp) {
+                const int r = tp / 3, sx = tp - 3 * (tp / 3);
+                // the 128B swizzle follows the absolute shared-memory address (as the
+                // TMA wrote it), so a view starting s rows into a swizzle atom needs
+                // no base offset (measured: base offset s gives wrong products)
+                const uint64_t ta =
+                    sdesc_sw128(abase + (uint32_t)((r * 16 + sx) * 128), 16, 2048);
+                const uint32_t tb = smem_u32(resB + tp * C::B_BYTES);
+                const uint64_t tbd = kBmn ? sdesc_sw128(tb, 8192, 1024) : sdesc_sw128(tb, 16, 1024);
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  mma_f16(d, ta + (uint64_t)(kk * kDA), tbd + (uint64_t)(kk * kDB), IDESC,
+                          (tp | kk) != 0);
+              }
+              mma_commit(&empty[s]);
+            }
+          } else if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t da = da0 + (uint64_t)(kk * kDA);
@@ -693,10 +721,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = wq * 32 + lane;
       const int m = m0 + row;
       int ex0 = 0, ey0 = 0, en0 = 0;
-      if (AM == A_TILE4) sp_origin(a, m0 / BM, ex0, ey0, en0);
-      const bool mv = AM == A_TILE4 ? m0 / BM < a.sp_tiles : m < a.M;
+      if (kSp) sp_origin(a, m0 / BM, ex0, ey0, en0);
+      // A_HALO tiles overhang the grid bottom: rows past the last image row are idle
+      const bool mv = kSp ? (m0 / BM < a.sp_tiles &&
+                             (AM != A_HALO || ey0 + row / a.sbw < a.sgh))
+                          : m < a.M;
       int64_t orow = m;
-      if (AM == A_TILE4) {  // tile row -> output pixel (x fastest, then y, then image)
+      if (kSp) {  // tile row -> output pixel (x fastest, then y, then image)
         const int bx = row % a.sbw, t2 = row / a.sbw;
         orow = ((int64_t)(en0 + t2 / a.sbh) * a.sgh + ey0 + t2 % a.sbh) * a.sgw + ex0 + bx;
       }
@@ -716,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* bb = stg + ew * kStgBufs * 4096 + (k & 1) * 2048;
           bulk_wait_read<0>();  // this half's previous store has read it
           mbar_arrive_tx(&ebar[ew * 2 + (k & 1)], 2048);
-          if (AM == A_TILE4) {
+          if (kSp) {
             const int rr = 32 * wq, t2 = rr / a.sbw;
             tma_load_4d(bb, &tmC, &ebar[ew * 2 + (k & 1)], n0 + cc, ex0 + rr % a.sbw,
                         ey0 + t2 % a.sbh, en0 + t2 / a.sbh);
@@ -734,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t* bar = &ebar[ew * 2 + (k & 1)];
           bulk_wait_read<0>();  // this set's previous store has read it
           mbar_arrive_tx(bar, 2048u * (1u + (a.bn_gate ? 1u : 0u) + (a.acc ? 1u : 0u)));
-          if (AM == A_TILE4) {
+          if (kSp) {
             const int rr = 32 * wq, t2 = rr / a.sbw;
             const int cx = ex0 + rr % a.sbw, cy = ey0 + t2 % a.sbh, cn = en0 + t2 / a.sbh;
             tma_load_4d(bb, &em.x, bar, n0 + cc, cx, cy, cn);
@@ -830,7 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            if (AM == A_TILE4) {
+            if (kSp) {
               const int rr = 32 * wq, t2 = rr / a.sbw;
               tma_store_4d(&em.o, bs, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
                            en0 + t2 / a.sbh);
@@ -877,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            if (AM == A_TILE4) {
+            if (kSp) {
               const int rr = 32 * wq, t2 = rr / a.sbw;
               tma_store_4d(&tmC, buf, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
                            en0 + t2 / a.sbh);
@@ -928,7 +959,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            if (AM == A_TILE4) {  // the warp's 32 rows are a sub-box of the pixel box
+            if (kSp) {  // the warp's 32 rows are a sub-box of the pixel box
               const int rr = 32 * wq, t2 = rr / a.sbw;
               tma_store_4d(&tmC, buf, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
                            en0 + t2 / a.sbh);
@@ -1500,12 +1531,33 @@ struct Plan {
   bool sp = false;
   int sbw = 0, sbh = 0, sbi = 0, stw = 0, sth = 0, sp_tiles = 0, slw = 0, slh = 0;
   int sgw = 0, sgh = 0;
+  bool halo = false;     // A_HALO (see the enum)
   const void* sp_a = nullptr;  // tensor of the A boxes: dims (sp_ac, sgw, sgh, n)
   const void* sp_b = nullptr;  // wgrad B boxes: dims (sp_bc, bw_, bh_, n)
   int sp_ac = 0, sp_bc = 0, sp_bw = 0, sp_bh = 0, sp_n = 0;
 };
 
 static bool use_tile4() { return nnl_set_tc_tile4(-1) >= 1; }
+
+static int halo_mode() { return nnl_set_tc_halo(-1); }
+
+// 3x3 / stride 1 / pad 1 over one 64-channel block with a 64-wide output: the
+// (8 x 16) pixel tiles of A_HALO (grid width a multiple of 8)
+static bool halo_layout(const ConvGeom& g, int cin, int w, int h, const void* src, int cout,
+                        Plan& pl) {
+  if (!halo_mode() || g.r != 3 || g.s != 3 || g.sh != 1 || g.sw != 1 || g.ph != 1 ||
+      g.pw != 1 || cin != 64 || cout != 64 || w % 8 || w > 256 || h > 256)
+    return false;
+  pl.halo = true; pl.sp = true;
+  pl.amode = A_HALO; pl.cblk = 1;
+  pl.sbw = 8; pl.sbh = 16; pl.sbi = 1;
+  pl.stw = w / 8; pl.sth = (h + 15) / 16;
+  pl.sp_tiles = pl.stw * pl.sth * g.n;
+  pl.slw = -1; pl.slh = -1; pl.sgw = w; pl.sgh = h;
+  pl.sp_a = src; pl.sp_ac = 64; pl.sp_bw = w; pl.sp_bh = h; pl.sp_n = g.n;
+  pl.M = pl.sp_tiles * BM;
+  return true;
+}
 // accumulate-mode outputs through TMA load/store (env NNL_TMA_ACC=0: direct stores)
 static bool use_tma_acc_env() {
   static int v = -1;
@@ -1713,6 +1765,8 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       pl.bmode = B_TMA_K; pl.B = {pb.b, g.k, rsc, rsc};
       if (one) {
         pl.amode = A_TMA_K; pl.A = {pb.a, nhw, g.c, g.c};
+      } else if (!pb.bnx && halo_layout(g, g.c, g.q, g.p, pb.a, g.k, pl)) {
+        // A_HALO: B = the nine taps' weights, resident
       } else if (use_tile4() && g.sh == 1 && g.sw == 1 && sp_box(g.q, g.p, g.n, BM, pl)) {
         pl.sp = true;
         pl.amode = A_TILE4; pl.cblk = g.c / 64;
@@ -1768,6 +1822,8 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       pl.amode = A_IM2COL; pl.cblk = g.k / 64;
       pl.im = {pb.a, g.k, g.q, g.p, g.n, pl.ilw, pl.ilh, pl.gw - g.q + pl.ilw,
                pl.gh - g.p + pl.ilh, 1, 1, BM};
+    } else if (!pb.bnx && halo_layout(g, g.k, g.w, g.h, pb.a, g.c, pl)) {
+      pl.flip = 1;  // dgrad: tap t uses weight tap 8 - t (resident B)
     } else if (g.sh == 1 && g.sw == 1 && use_tile4() && sp_box(g.w, g.h, g.n, BM, pl)) {
       // stride-1 dgrad over spatial tiles of dx: tap t reads dy at
       // (x + s + pw-(S-1), y + r + ph-(R-1)) with weight tap R*S-1-t
@@ -1835,7 +1891,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   pl.bn = pick_bn(pl, pl.bmode == B_TMA_MN && pl.b_tap_stride && !k1);
   if (pb.bnx && pl.bn > 128) pl.bn = 128;  // the fused BN-backward epilogue's smem budget
   if (pl.remap && pl.N % pl.bn) pl.bn = 64;
-  pl.num_kb = (int)cdiv(pl.K, BK);
+  pl.num_kb = pl.halo ? 1 : (int)cdiv(pl.K, BK);  // A_HALO: one ring stage per tile
   auto tile_and_split = [&](int cg) {
     pl.cg = cg;
     pl.tiles_m = (int)cdiv(pl.M, BM * cg);
@@ -1844,7 +1900,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     // split the reduction when the tile grid cannot fill the machine
     int splits = 1;
     const int sms = num_sms() / cg;  // concurrent work slots (CTAs or CTA pairs)
-    if (tiles < sms && pb.stats == nullptr && !pl.remap && pl.amode != A_TILE4) {
+    if (tiles < sms && pb.stats == nullptr && !pl.remap && pl.amode != A_TILE4 && !pl.halo) {
       // wave-quantisation-aware choice: cost in k-block times of the busiest
       // slot (waves x (k-blocks per unit + epilogue)) plus the f32 partial
       // round trip of the fixed-order reduction (~0.26 us per k-block at
@@ -1887,8 +1943,9 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
     const bool b_ok = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN;
     const bool a_ok = pl.amode == A_TMA_K || pl.amode == A_IM2COL || pl.amode == A_IM2COL16 ||
                       pl.amode == A_TILE4;
-    pl.resb = use_resident_b() && b_ok && a_ok && pl.cg == 1 && pl.tiles_n == 1 && !pb.bnx &&
-            pl.splits == 1 && (int64_t)pl.num_kb * pl.bn * BK * 2 <= RES_MAX;
+    pl.resb = pl.halo || (use_resident_b() && b_ok && a_ok && pl.cg == 1 && pl.tiles_n == 1 &&
+                          !pb.bnx && pl.splits == 1 &&
+                          (int64_t)pl.num_kb * pl.bn * BK * 2 <= RES_MAX);
   }
   if (pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad))
     pl.ws_partial = (size_t)pl.splits * pl.M * pl.N * 4;
@@ -1906,7 +1963,7 @@ static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& t
                      const CUtensorMap& tc, const EpiMaps& em, const TcArgs& args,
                      cudaStream_t st) {
   auto kern = k_tc_gemm<BN, AM, BMD, CG, RB, EP>;
-  using C = Cfg<BN, CG, RB, EP>;
+  using C = Cfg<BN, CG, RB, EP, AM == A_HALO>;
   static bool attr = false;
   if (!attr) {
     NNL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1973,6 +2030,10 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   NNL_TC_CASE(A_TILE4, B_TMA_K)
   NNL_TC_CASE(A_TILE4, B_TMA_MN)
   NNL_TC_CASE(A_TILE4MN, B_TILE4)
+  if constexpr (BN == 64) {
+    NNL_TC_CASE_RB(A_HALO, B_TMA_K)
+    NNL_TC_CASE_RB(A_HALO, B_TMA_MN)
+  }
   NNL_TC_CASE_RB(A_TILE4, B_TMA_K)
   NNL_TC_CASE_RB(A_TILE4, B_TMA_MN)
   NNL_TC_CASE_RB(A_TMA_K, B_TMA_K)
@@ -2141,7 +2202,10 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   memset(&ta, 0, sizeof(ta));
   memset(&tb, 0, sizeof(tb));
   int rc;
-  if (pl.amode == A_TILE4) {
+  if (pl.amode == A_HALO) {  // 16 x 18 halo pixels (10 x 18 used) per tile
+    const int box[4] = {64, 16, pl.sbh + 2, 1};
+    if ((rc = make_tmap4(&ta, pl.sp_a, pl.sp_ac, pl.sp_bw, pl.sp_bh, pl.sp_n, box))) return rc;
+  } else if (pl.amode == A_TILE4) {
     const int box[4] = {64, pl.sbw, pl.sbh, pl.sbi};
     if ((rc = make_tmap4(&ta, pl.sp_a, pl.sp_ac, pl.sp_bw, pl.sp_bh, pl.sp_n, box))) return rc;
   } else if (pl.amode == A_TILE4MN) {
@@ -2194,6 +2258,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   args.sbw = pl.sbw; args.sbh = pl.sbh; args.sbi = pl.sbi; args.stw = pl.stw; args.sth = pl.sth;
   args.sp_tiles = pl.sp_tiles; args.slw = pl.slw; args.slh = pl.slh;
   args.sgw = pl.sgw; args.sgh = pl.sgh;
+  args.res_kb = pl.halo ? 9 : 0;
   args.c4_s2 = pl.c4_s2; args.c4_w4 = pl.c4_w4; args.c4_off = pl.c4_off; args.c4_pair = pl.c4_pair;
   const bool to_partial = pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad);
   args.partial = to_partial ? partial : nullptr;
@@ -2216,7 +2281,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
                         pl.bmode == B_GATHER_C4;
     const bool cw32 = (!gather && pl.bn == 64) || args.acc;  // acc: 32-column chunks
     const CUtensorMapSwizzle sw = cw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-    if (pl.amode == A_TILE4) {  // 32-row sub-boxes of the pixel box over the output grid
+    if (pl.amode == A_TILE4 || pl.amode == A_HALO) {  // 32-row sub-boxes over the output grid
       const int bw32 = pl.sbw < 32 ? pl.sbw : 32;
       const int bh32 = pl.sbh < 32 / bw32 ? pl.sbh : 32 / bw32;
       const int box[4] = {cw32 ? 32 : 64, bw32, bh32, 32 / (bw32 * bh32)};

@@ -28,6 +28,8 @@ CONV = [  # (B, cin, cout, k, stride, pad, hw)
     (4, 256, 512, 1, 2, 0, 14),    # 1x1 s2 dgrad: row remap + zero fill
     (16, 128, 256, 3, 1, 1, 14),   # 3x3 gather with 256-wide tiles
     (64, 64, 128, 3, 1, 1, 20),    # > 148 work units: persistent tile loop
+    (4, 64, 64, 3, 1, 1, 24),      # shared-halo tiles, last tile row past the image
+    (2, 64, 64, 3, 1, 1, 56),      # shared-halo tiles at the ResNet-50 stage-1 extent
     (4, 64, 128, 3, 2, 1, 16),     # strided 3x3 dgrad: 4 parity-class GEMMs
     (2, 64, 64, 3, 1, 0, 9),       # valid (pad 0) 3x3: dgrad im2col bounding box
 ]
@@ -368,3 +370,35 @@ def test_dgrad_bn_stats_epilogue(nnl, geom, tail):
     sums = parts.cpu().numpy().reshape(rows, 2, cin).sum(0)
     want = np.stack([gy.sum(0, dtype=np.float64), (gy * xh).sum(0, dtype=np.float64)])
     np.testing.assert_allclose(sums, want, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("geom", [(4, 64, 64, 3, 1, 1, 56), (3, 64, 64, 3, 1, 1, 24),
+                                  (8, 64, 64, 3, 1, 1, 16)])
+def test_halo_tiles_match_per_tap_loads(nnl, geom):
+    """3x3 convolutions over one shared input halo per tile (nine descriptor views
+    into it) against per-tap operand loads: same (tap, K16) MMA order, outputs
+    and input gradients agree to f32 accumulation rounding (the per-tap path may
+    split K on small grids)."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    b, cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(14)
+    x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (cout, cin, k, k)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, (cout,)).astype(np.float32)
+    outs = []
+    for mode in (1, 0):
+        prev = _lib.lib().nnl_set_tc_halo(mode)
+        try:
+            vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+            for v, a in zip(vs, (x, w, bias)):
+                v.d = a
+            y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+            y.forward()
+            y.backward(1.0)
+            outs.append([y.d, vs[0].g])
+        finally:
+            _lib.lib().nnl_set_tc_halo(prev)
+    for a, c in zip(outs[0], outs[1]):
+        assert _rel_err(a, c) < 2e-3
