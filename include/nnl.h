@@ -131,6 +131,12 @@ int nnl_conv2d_bwd_data(const nnl_conv_shape* cs, int dtype, const void* dy, con
 int nnl_conv2d_bwd_weight(const nnl_conv_shape* cs, int dtype, const void* x, const void* dy,
                           void* dw, int acc_w, void* db, int acc_b, int32_t* nonfinite,
                           void* ws, size_t ws_bytes, void* stream);
+/* Thread-local opt-in (returns the previous value, < 0 only queries): the next
+   nnl_conv2d_bwd_weight calls may reuse the space-to-depth copy of x that the
+   forward of the same convolution built in the SAME workspace, skipping its
+   rebuild.  The caller guarantees that workspace was not used in between (the
+   engine gives the stem its own workspace) and that x is unchanged. */
+int nnl_conv2d_prep_reuse(int enabled);
 /* number of stat-partial rows nnl_conv2d_fwd writes (0 if fusion unsupported) */
 int32_t nnl_conv2d_stat_rows(const nnl_conv_shape* cs, int dtype);
 

@@ -310,6 +310,12 @@ int nnl_set_tc_tile4(int enabled) {
   if (enabled >= 0) v = enabled > 2 ? 2 : enabled;
   return prev;
 }
+int nnl_conv2d_prep_reuse(int enabled) {
+  static thread_local int v = 0;
+  const int prev = v;
+  if (enabled >= 0) v = enabled ? 1 : 0;
+  return prev;
+}
 int nnl_set_tc_halo(int enabled) {
   static int v = -1;
   if (v < 0) {

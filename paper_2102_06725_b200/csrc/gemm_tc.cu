@@ -2142,8 +2142,25 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     NNL_CHECK_LAUNCH();
     if (pb.mode == kFprop) pl.A.ptr = col; else pl.B.ptr = col;
   }
-  if (pl.s2d) {
-    const __half* src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
+  // the space-to-depth copy built by a forward stays valid in that workspace for
+  // the weight gradient when the caller guarantees nothing else used it in between
+  // (nnl_conv2d_prep_reuse, a per-node workspace)
+  struct PrepKey {
+    const void* xs; const void* src; int n, h, w, c, ph, pw;
+  };
+  static thread_local PrepKey last_prep = {};
+  const __half* prep_src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
+  const PrepKey key = {xs, prep_src, g.n, g.h, g.w, g.c, g.ph, g.pw};
+  const bool prep_hit = pl.s2d && pb.mode == kWgrad && nnl_conv2d_prep_reuse(-1) == 1 &&
+                        memcmp(&key, &last_prep, sizeof(key)) == 0;
+  if (pl.s2d && prep_hit) {  // one use per forward build
+    pl.im.ptr = xs;
+    last_prep = PrepKey{};
+  }
+  if (pl.s2d && !prep_hit) {
+    const __half* src = prep_src;
+    if (pb.mode == kFprop) last_prep = key;
+    else last_prep = PrepKey{};
     const int64_t pix = (int64_t)g.n * pl.g2.h * pl.g2.w;
     if (pix >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "space-to-depth input too large");
     const bool rows = pl.s2d4 && g.w * g.c * 4 <= 48 * 1024;

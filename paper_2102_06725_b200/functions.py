@@ -199,6 +199,16 @@ class Convolution(FunctionImpl):
         cs = self.shape_struct(x.shape)
         return int(_lib.lib().nnl_conv2d_stat_rows(C.byref(cs), x.code))
 
+    def _workspace(self, node, cs, code, pass_):
+        """The shared workspace, or for narrow-channel inputs (the stem) the node's
+        own, so that the weight gradient can reuse the space-to-depth copy of x
+        its forward built there (nnl_conv2d_prep_reuse)."""
+        if node.inputs[0].shape[1] > 4:
+            return _lib.workspace(_lib.lib().nnl_conv2d_workspace_size(C.byref(cs), code, pass_))
+        n = max(int(_lib.lib().nnl_conv2d_workspace_size(C.byref(cs), code, p)) for p in (0, 2))
+        buf = _state_buf(node, "ws_own", (n + 3) // 4)
+        return buf.data_ptr(), buf.numel() * 4
+
     def forward(self, node, xs, ys):
         x, w, b = xs
         cs = self.shape_struct(x.shape)
@@ -210,7 +220,7 @@ class Convolution(FunctionImpl):
                 node.state["stat_rows"] = rows
             else:
                 node.state.pop("emit_stats", None)
-        ws = _lib.workspace(_lib.lib().nnl_conv2d_workspace_size(C.byref(cs), x.code, 0))
+        ws = self._workspace(node, cs, x.code, 0)
         _lib.call("nnl_conv2d_fwd", C.byref(cs), x.code, x.ptr, w.ptr, b.ptr, ys[0].ptr,
                   stats.data_ptr() if stats is not None else None, ws[0], ws[1], _st())
 
@@ -261,11 +271,18 @@ class Convolution(FunctionImpl):
         # the bias gradient was already reduced by the following BN's backward
         gb = None if node.state.get("bias_by_bn") else gxs[2]
         if gxs[1] is not None or gb is not None:
-            ws = _lib.workspace(_lib.lib().nnl_conv2d_workspace_size(C.byref(cs), x.code, 2))
-            _lib.call("nnl_conv2d_bwd_weight", C.byref(cs), x.code, x.ptr, gy.ptr,
-                      gxs[1].ptr if gxs[1] is not None else None, _flag(acc[1]),
-                      gb.ptr if gb is not None else None, _flag(acc[2]),
-                      node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
+            own = x.shape[1] <= 4
+            ws = self._workspace(node, cs, x.code, 2)
+            if own:
+                _lib.lib().nnl_conv2d_prep_reuse(1)
+            try:
+                _lib.call("nnl_conv2d_bwd_weight", C.byref(cs), x.code, x.ptr, gy.ptr,
+                          gxs[1].ptr if gxs[1] is not None else None, _flag(acc[1]),
+                          gb.ptr if gb is not None else None, _flag(acc[2]),
+                          node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
+            finally:
+                if own:
+                    _lib.lib().nnl_conv2d_prep_reuse(0)
 
     def backward_reads_input(self, index):
         return index in (0, 1)
