@@ -698,13 +698,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int t = 0;
     uint32_t sb = 0;  // TMA-store staging buffer alternation (per warp)
     uint32_t ac = 0;  // accumulate mode: chunks processed by this warp (2 KB buffers)
+    int staged_n0 = -1;  // N tile whose bias slice is in bias_s
     // the leader's tempty barriers (the MMA waits on both CTAs' epilogues)
     const uint32_t te0 = CG == 2 ? mapa_shared(&tempty[0], 0) : smem_u32(&tempty[0]);
     for (int u = pair; u < a.units; u += npairs, ++t) {
       const Unit w = decode_unit(a, u);
       const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN;
       const int ab = t & 1;
-      if (a.bias || EP == 1) {  // this tile's bias / BN slices, staged once (as f32)
+      if ((a.bias || EP == 1) && n0 != staged_n0) {  // bias / BN slices of this N tile (f32)
+        staged_n0 = n0;
         named_sync(2, kEpiThreads);
         for (int j = tid; j < BN; j += kEpiThreads) {
           const bool ok = n0 + j < a.N;
@@ -783,6 +785,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[ab], (t >> 1) & 1);
       tc_fence_after();
       int bad = 0;
+      // the accumulator buffer is handed back to the MMA warp as soon as this
+      // warp's last TMEM load of the tile has completed (the rest of the
+      // epilogue works from registers / shared memory)
+      bool released = false;
+      auto release_tmem = [&](bool last) {
+        if (!last || released) return;
+        released = true;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(te0 + 8 * ab);
+          else mbar_arrive(&tempty[ab]);
+        }
+      };
       if (EP == 1) {
         // fused BN backward (TcArgs::bnx): row `lane`, 8 columns per 16 B piece;
         // g = q(prev + acc), gy = g * gate, out = q(gy) written over the x tile and
@@ -792,6 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t v[32];
           tmem_ld32_nowait(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
           tmem_wait_ld();
+          release_tmem(c + 32 >= c_hi);
           uint8_t* bs = stg + ew * 12288 + (ac & 1) * 6144;
           mbar_wait(&ebar[ew * 2 + (ac & 1)], (ac >> 1) & 1);
           const int swz = (lane >> 1) & 3;
@@ -877,6 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t v[32];
           tmem_ld32_nowait(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
           tmem_wait_ld();
+          release_tmem(c + 32 >= c_hi);
           uint8_t* buf = stg + ew * kStgBufs * 4096 + (ac & 1) * 2048;
           mbar_wait(&ebar[ew * 2 + (ac & 1)], (ac >> 1) & 1);
           const int swz = (lane >> 1) & 3;  // 64 B rows, 64 B swizzle
@@ -928,6 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32_nowait(tb, v);
           if (CW == 64) tmem_ld32_nowait(tb + 32, v + 32);
           tmem_wait_ld();
+          release_tmem(c + CW >= c_hi);
           uint8_t* buf = stg + (ew * kStgBufs + (sb % kStgBufs)) * 4096;
           ++sb;
           if (lane == 0) bulk_wait_read<kStgBufs - 1>();  // buf's previous store has read it
@@ -1005,6 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[32];
         tmem_ld32_nowait(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ab * BN + c), v);
         tmem_wait_ld();
+        release_tmem(c + 32 >= c_hi);
         const int nb = n0 + c;
         const bool full_cols = nb + 32 <= a.N;
         if (a.partial) {
@@ -1100,13 +1120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      // the accumulator buffer can be reused by the MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(te0 + 8 * ab);
-        else mbar_arrive(&tempty[ab]);
-      }
+      release_tmem(true);  // (a warp with no columns in this tile)
       if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
       if (a.stats) {
         named_sync(1, kEpiThreads);
