@@ -699,6 +699,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t sb = 0;  // TMA-store staging buffer alternation (per warp)
     uint32_t ac = 0;  // accumulate mode: chunks processed by this warp (2 KB buffers)
     int staged_n0 = -1;  // N tile whose bias slice is in bias_s
+    // BN statistics of a single-N-tile GEMM stored through TMA: each warp keeps its
+    // columns' running sums in registers over all its tiles (fixed tile order) and
+    // the four row-quarter warps are combined once at the end -- no per-tile barrier
+    const bool reg_stats = a.stats && a.tma_store && a.tiles_n == 1;
+    float racc[4][4] = {};
     // the leader's tempty barriers (the MMA waits on both CTAs' epilogues)
     const uint32_t te0 = CG == 2 ? mapa_shared(&tempty[0], 0) : smem_u32(&tempty[0]);
     for (int u = pair; u < a.units; u += npairs, ++t) {
@@ -999,11 +1004,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 s2a += x.x * x.x;
                 s2b += x.y * x.y;
               }
-              float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
-              rp[0] = s1a;
-              rp[1] = s2a;
-              rp[2] = s1b;
-              rp[3] = s2b;
+              if (reg_stats) {
+                float* ra = racc[(c - c_lo) / CW];
+                ra[0] += s1a; ra[1] += s2a; ra[2] += s1b; ra[3] += s2b;
+              } else {
+                float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
+                rp[0] = s1a;
+                rp[1] = s2a;
+                rp[2] = s1b;
+                rp[3] = s2b;
+              }
             } else {  // lane owns column c + lane
               float s1 = 0.f, s2 = 0.f;
 #pragma unroll 8
@@ -1013,9 +1023,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 s1 += x;
                 s2 += x * x;
               }
-              float* rp = red + ((wq * BN) + c + lane) * 2;
-              rp[0] = s1;
-              rp[1] = s2;
+              if (reg_stats) {
+                float* ra = racc[(c - c_lo) / CW];
+                ra[0] += s1; ra[1] += s2;
+              } else {
+                float* rp = red + ((wq * BN) + c + lane) * 2;
+                rp[0] = s1;
+                rp[1] = s2;
+              }
             }
           }
         }
@@ -1122,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       release_tmem(true);  // (a warp with no columns in this tile)
       if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
-      if (a.stats) {
+      if (a.stats && !reg_stats) {
         named_sync(1, kEpiThreads);
         for (int col = tid; col < BN; col += kEpiThreads) {
           if (n0 + col >= a.N) continue;
@@ -1138,6 +1153,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_sync(1, kEpiThreads);
       }
+    }
+    if (reg_stats) {  // combine the row-quarter warps: red[q][col] -> stat_s[col]
+      for (int k = 0; k * CW < c_hi - c_lo; ++k) {
+        const int c = c_lo + k * CW;
+        if (CW == 64) {
+          float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
+          rp[0] = racc[k][0]; rp[1] = racc[k][1]; rp[2] = racc[k][2]; rp[3] = racc[k][3];
+        } else {
+          float* rp = red + ((wq * BN) + c + lane) * 2;
+          rp[0] = racc[k][0]; rp[1] = racc[k][1];
+        }
+      }
+      named_sync(1, kEpiThreads);
+      for (int col = tid; col < BN && col < a.N; col += kEpiThreads) {
+        float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          t1 += red[(q * BN + col) * 2 + 0];
+          t2 += red[(q * BN + col) * 2 + 1];
+        }
+        stat_s[col] = t1;
+        stat_s[C::MAX_STAT_N + col] = t2;
+      }
+      named_sync(1, kEpiThreads);
     }
     if (a.stats) {  // one partial row per CTA: stats[blockIdx.x][2][N]
       for (int col = tid; col < a.N; col += kEpiThreads) {
