@@ -48,8 +48,9 @@ enum AMode {
   A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FPROP = 2, A_GATHER_DGRAD = 3, A_IM2COL = 4,
   A_GATHER_C4 = 5, A_IM2COL16 = 6, A_TILE4 = 7, A_TILE4MN = 8, A_HALO = 9
 };
-// A_HALO: 3x3 stride-1 pad-1 convolutions over 64 channels (one channel block):
-// the (8 x 16)-pixel M tile's input halo (10 x 18 pixels, rows padded to 16 pixels)
+// A_HALO: stride-1 convolutions over 64 channels (one channel block) -- the 3x3
+// pad-1 layers and the stem's 4x1 convolution over x4: the (8 x 16)-pixel M tile's
+// input halo (3x3: 10 x 18 pixels, rows padded to a 16-pixel pitch; stem: 8 x 19)
 // is ONE tiled 4D TMA box per tile, and the nine taps are nine descriptor views
 // into it (view (r, s) starts at halo row r*16 + s: SBO 2048 B, no base offset),
 // so each input pixel crosses L2 -> SMEM once per tile instead of once per tap.
@@ -136,7 +137,9 @@ struct TcArgs {
   // (r, s) of a box at (x0, y0, n0) reads input (x0 + s + slw, y0 + r + slh, n0);
   // the epilogue's output grid is sgw x sgh (A_TILE4: rows -> pixels, 4D store)
   int sbw, sbh, sbi, stw, sth, sp_tiles, slw, slh, sgw, sgh;
-  int res_kb;         // resident-B k-blocks when they differ from num_kb (A_HALO: 9 taps)
+  int res_kb;         // resident-B k-blocks when they differ from num_kb (A_HALO: taps)
+  int hl_pitch, hl_r, hl_s;  // A_HALO: halo row pitch (pixels) and filter taps R x S
+  uint32_t hl_bytes;  // A_HALO: bytes of one halo box
   // fused BatchNormalization backward statistics (dgrad of the convolution
   // after a BN[+ReLU]): g = the rounded dgrad output; gy = g * gate with gate
   // = (bn_gate > 0) (residual tail) or (q(gamma*xhat + beta) > 0) (bn_relu),
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kb = w.kb0 + i;
           mbar_wait(&empty[s], ph ^ 1);
           // the leader's barrier counts both CTAs' bytes; the peer only loads
-          if (rank == 0) mbar_arrive_tx(&full[s], kTmaBytes * CG);
+          if (rank == 0) mbar_arrive_tx(&full[s], AM == A_HALO ? a.hl_bytes : kTmaBytes * CG);
           const uint32_t fb = CG == 2 ? mapa_shared(&full[s], 0) : smem_u32(&full[s]);
           auto load2d = [&](void* dst, const CUtensorMap* tm, int c0, int c1) {
             if (CG == 2) tma_load_2d_cg2(dst, tm, fb, c0, c1);
@@ -464,13 +467,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       : sdesc_sw128(bbase, 16, 1024);
           if (AM == A_HALO) {
             if (elect_one()) {
-              for (int tp = 0; tp < 9; ++tp) {
-                const int r = tp / 3, sx = tp - 3 * (tp / 3);
+              for (int tp = 0; tp < a.hl_r * a.hl_s; ++tp) {
+                const int r = tp / a.hl_s, sx = tp - a.hl_s * r;
                 // the 128B swizzle follows the absolute shared-memory address (as the
                 // TMA wrote it), so a view starting s rows into a swizzle atom needs
                 // no base offset (measured: base offset s gives wrong products)
-                const uint64_t ta =
-                    sdesc_sw128(abase + (uint32_t)((r * 16 + sx) * 128), 16, 2048);
+                const uint64_t ta = sdesc_sw128(
+                    abase + (uint32_t)((r * a.hl_pitch + sx) * 128), 16,
+                    (uint32_t)a.hl_pitch * 128u);
                 const uint32_t tb = smem_u32(resB + tp * C::B_BYTES);
                 const uint64_t tbd = kBmn ? sdesc_sw128(tb, 8192, 1024) : sdesc_sw128(tb, 16, 1024);
 #pragma unroll
@@ -1585,6 +1589,7 @@ struct Plan {
   int sbw = 0, sbh = 0, sbi = 0, stw = 0, sth = 0, sp_tiles = 0, slw = 0, slh = 0;
   int sgw = 0, sgh = 0;
   bool halo = false;     // A_HALO (see the enum)
+  int hl_pitch = 16, hl_r = 3, hl_s = 3;
   const void* sp_a = nullptr;  // tensor of the A boxes: dims (sp_ac, sgw, sgh, n)
   const void* sp_b = nullptr;  // wgrad B boxes: dims (sp_bc, bw_, bh_, n)
   int sp_ac = 0, sp_bc = 0, sp_bw = 0, sp_bh = 0, sp_n = 0;
@@ -1840,6 +1845,20 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       pl.amode = pl.s2d4 ? A_IM2COL : A_IM2COL16;
       pl.bmode = B_TMA_K; pl.B = {nullptr, g.k, pl.kp, pl.kp};
       pl.ws_wpad = (size_t)g.k * pl.kp * 2;
+      // the R2 x 1 convolution over x4 from one halo per (8 x 16)-pixel tile:
+      // 8-pixel rows, so the tap views start on swizzle-atom boundaries
+      if (pl.s2d4 && halo_mode() && g.k == 64 && g.q % 8 == 0 &&
+          pl.g2.r + 15 <= 256) {
+        pl.halo = true; pl.sp = true;
+        pl.amode = A_HALO; pl.cblk = 1;
+        pl.hl_pitch = 8; pl.hl_r = pl.g2.r; pl.hl_s = 1;
+        pl.sbw = 8; pl.sbh = 16; pl.sbi = 1;
+        pl.stw = g.q / 8; pl.sth = (g.p + 15) / 16;
+        pl.sp_tiles = pl.stw * pl.sth * g.n;
+        pl.slw = 0; pl.slh = 0; pl.sgw = g.q; pl.sgh = g.p;
+        pl.sp_ac = 64; pl.sp_bw = pl.g2.w; pl.sp_bh = pl.g2.h; pl.sp_n = g.n;
+        pl.M = pl.sp_tiles * BM;
+      }
     } else if (g.c <= 4) {
       c4_layout(g, pl);
       pl.K = pl.kp;
@@ -2208,6 +2227,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
                         memcmp(&key, &last_prep, sizeof(key)) == 0;
   if (pl.s2d && prep_hit) {  // one use per forward build
     pl.im.ptr = xs;
+    pl.sp_a = xs;
     last_prep = PrepKey{};
   }
   if (pl.s2d && !prep_hit) {
@@ -2230,6 +2250,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
           g.n, g.h, g.w, g.c, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
     NNL_CHECK_LAUNCH();
     pl.im.ptr = xs;
+    pl.sp_a = xs;
     if (pb.mode == kFprop) {
       const int total = g.k * pl.kp;
       k_w_s2d<<<grid_for(total, 256), 256, 0, st>>>(g.k, g.r, g.s, g.c, pl.g2.r, pl.s2,
@@ -2272,8 +2293,8 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   memset(&ta, 0, sizeof(ta));
   memset(&tb, 0, sizeof(tb));
   int rc;
-  if (pl.amode == A_HALO) {  // 16 x 18 halo pixels (10 x 18 used) per tile
-    const int box[4] = {64, 16, pl.sbh + 2, 1};
+  if (pl.amode == A_HALO) {  // pitch x (tile rows + R - 1) halo pixels per tile
+    const int box[4] = {64, pl.hl_pitch, pl.sbh + pl.hl_r - 1, 1};
     if ((rc = make_tmap4(&ta, pl.sp_a, pl.sp_ac, pl.sp_bw, pl.sp_bh, pl.sp_n, box))) return rc;
   } else if (pl.amode == A_TILE4) {
     const int box[4] = {64, pl.sbw, pl.sbh, pl.sbi};
@@ -2328,7 +2349,9 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   args.sbw = pl.sbw; args.sbh = pl.sbh; args.sbi = pl.sbi; args.stw = pl.stw; args.sth = pl.sth;
   args.sp_tiles = pl.sp_tiles; args.slw = pl.slw; args.slh = pl.slh;
   args.sgw = pl.sgw; args.sgh = pl.sgh;
-  args.res_kb = pl.halo ? 9 : 0;
+  args.res_kb = pl.halo ? pl.hl_r * pl.hl_s : 0;
+  args.hl_pitch = pl.hl_pitch; args.hl_r = pl.hl_r; args.hl_s = pl.hl_s;
+  args.hl_bytes = (uint32_t)(pl.hl_pitch * (pl.sbh + pl.hl_r - 1) * 128);
   args.c4_s2 = pl.c4_s2; args.c4_w4 = pl.c4_w4; args.c4_off = pl.c4_off; args.c4_pair = pl.c4_pair;
   const bool to_partial = pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad);
   args.partial = to_partial ? partial : nullptr;
