@@ -17,6 +17,7 @@ from . import _lib
 class _Profiler:
     def __init__(self):
         self.enabled = False
+        self.gpu_lead_cycles = 0  # > 0: spin the GPU this long before each region
         self.records = []  # (kind, phase, flops, bytes, start_event, end_event)
 
     def reset(self):
@@ -30,6 +31,10 @@ class _Profiler:
         t = _lib.torch()
         s = t.cuda.Event(enable_timing=True)
         e = t.cuda.Event(enable_timing=True)
+        if self.gpu_lead_cycles:
+            # keep the GPU busy while the host enqueues this node, so the events
+            # time the node's kernels, not the host's launch latency
+            t.cuda._sleep(self.gpu_lead_cycles)
         s.record()
         yield
         e.record()
