@@ -114,6 +114,8 @@ __global__ void k_scaler_finish(nnl_scaler_state* s) {
   s->nonfinite = 0;
 }
 
+// 4 elements per thread when the chunk, its bucket position and its start are
+// 4-aligned (every chunk of a parameter whose size is a multiple of 4), else scalar
 __global__ void k_bucket_pack(const nnl_param_slot* __restrict__ slots,
                               const nnl_chunk* __restrict__ chunks,
                               const int64_t* __restrict__ pos, int32_t n_chunks,
@@ -121,11 +123,32 @@ __global__ void k_bucket_pack(const nnl_param_slot* __restrict__ slots,
   for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
     const nnl_chunk ch = chunks[ci];
     const nnl_param_slot& p = slots[ch.slot];
-    for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x)
-      bucket[pos[ci] + j] = load_any(p.grad, p.dtype, ch.start + j);
+    const int64_t b0 = pos[ci];
+    if (((b0 | ch.start | ch.len) & 3) == 0) {
+      float4* dst = reinterpret_cast<float4*>(bucket + b0);
+      for (int32_t j = threadIdx.x; j < ch.len / 4; j += blockDim.x) {
+        float4 v;
+        if (p.dtype == NNL_F16) {
+          const uint2 u = reinterpret_cast<const uint2*>(
+              reinterpret_cast<const __half*>(p.grad) + ch.start)[j];
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+          v = make_float4(a.x, a.y, b.x, b.y);
+        } else {
+          v = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.grad) +
+                                              ch.start)[j];
+        }
+        dst[j] = v;
+      }
+    } else {
+      for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x)
+        bucket[b0 + j] = load_any(p.grad, p.dtype, ch.start + j);
+    }
   }
 }
 
+// g = q(sum / f32(n)) into the gradient storage (communicator.py:99-105), OR of
+// non-finite results into the overflow flag
 __global__ void k_bucket_unpack(const nnl_param_slot* __restrict__ slots,
                                 const nnl_chunk* __restrict__ chunks,
                                 const int64_t* __restrict__ pos, int32_t n_chunks,
@@ -134,10 +157,33 @@ __global__ void k_bucket_unpack(const nnl_param_slot* __restrict__ slots,
   for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
     const nnl_chunk ch = chunks[ci];
     const nnl_param_slot& p = slots[ch.slot];
-    for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x) {
-      float v = __fdiv_rn(bucket[pos[ci] + j], world);  // acc /= f32(n)
-      store_any(p.grad, p.dtype, ch.start + j, v);
-      bad |= !isfinite(load_any(p.grad, p.dtype, ch.start + j));
+    const int64_t b0 = pos[ci];
+    if (((b0 | ch.start | ch.len) & 3) == 0) {
+      const float4* src = reinterpret_cast<const float4*>(bucket + b0);
+      for (int32_t j = threadIdx.x; j < ch.len / 4; j += blockDim.x) {
+        const float4 s4 = src[j];
+        const float v0 = __fdiv_rn(s4.x, world), v1 = __fdiv_rn(s4.y, world);
+        const float v2 = __fdiv_rn(s4.z, world), v3 = __fdiv_rn(s4.w, world);
+        if (p.dtype == NNL_F16) {
+          const __half2 a = __floats2half2_rn(v0, v1), b = __floats2half2_rn(v2, v3);
+          uint2 u;
+          u.x = *reinterpret_cast<const uint32_t*>(&a);
+          u.y = *reinterpret_cast<const uint32_t*>(&b);
+          reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.grad) + ch.start)[j] = u;
+          const float2 fa = __half22float2(a), fb = __half22float2(b);
+          bad |= !isfinite(fa.x) | !isfinite(fa.y) | !isfinite(fb.x) | !isfinite(fb.y);
+        } else {
+          reinterpret_cast<float4*>(reinterpret_cast<float*>(p.grad) + ch.start)[j] =
+              make_float4(v0, v1, v2, v3);
+          bad |= !isfinite(v0) | !isfinite(v1) | !isfinite(v2) | !isfinite(v3);
+        }
+      }
+    } else {
+      for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x) {
+        float v = __fdiv_rn(bucket[b0 + j], world);  // acc /= f32(n)
+        store_any(p.grad, p.dtype, ch.start + j, v);
+        bad |= !isfinite(load_any(p.grad, p.dtype, ch.start + j));
+      }
     }
   }
   if (flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
