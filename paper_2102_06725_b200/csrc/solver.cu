@@ -69,6 +69,29 @@ __global__ void k_multi_sumsq(const nnl_param_slot* __restrict__ slots,
   }
 }
 
+// one parameter element of the update (solver.py:100-109 + Momentum/wd); g is the
+// gradient as stored, returned: the (unscaled, re-rounded) gradient to store back
+__device__ __forceinline__ float update_elem(float g, bool f16, bool scaled, float factor,
+                                             float& m, float* mom, float lr, float momentum,
+                                             float wd) {
+  if (scaled) {
+    // scale_grad rounds the unscaled gradient back into grad storage (R10)
+    g = __fmul_rn(g, factor);
+    if (f16) g = __half2float(__float2half_rn(g));
+  }
+  float gw = g;
+  if (wd != 0.f) gw = __fadd_rn(gw, __fmul_rn(wd, m));
+  float step = __fmul_rn(lr, gw);
+  if (mom) {
+    step = __fadd_rn(__fmul_rn(momentum, *mom), step);
+    *mom = step;
+  }
+  m = __fsub_rn(m, step);
+  return g;
+}
+
+// 4 elements per thread on 4-aligned chunks (16 B master / momentum accesses,
+// 8 or 16 B grad / data accesses), scalar otherwise
 __global__ void k_multi_update(const nnl_param_slot* __restrict__ slots,
                                const nnl_chunk* __restrict__ chunks, int32_t n_chunks, float lr,
                                float momentum, float wd, const nnl_scaler_state* scaler) {
@@ -77,25 +100,72 @@ __global__ void k_multi_update(const nnl_param_slot* __restrict__ slots,
     if (scaler->nonfinite) return;  // SkippedInfNan: bytes stay unchanged
     factor = (float)(1.0 / scaler->loss_scale);  // np.float32(1.0 / S)
   }
-  for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
-    const nnl_param_slot& p = slots[s];
-    float g = load_any(p.grad, p.dtype, i);
-    if (scaler) {
-      // scale_grad rounds the unscaled gradient back into grad storage (R10)
-      store_any(p.grad, p.dtype, i, __fmul_rn(g, factor));
-      g = load_any(p.grad, p.dtype, i);
+  const bool scaled = scaler != nullptr;
+  for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
+    const nnl_chunk ch = chunks[ci];
+    const nnl_param_slot& p = slots[ch.slot];
+    const bool f16 = p.dtype == NNL_F16;
+    if (((ch.start | ch.len) & 3) == 0) {
+      for (int32_t j = threadIdx.x; j < ch.len / 4; j += blockDim.x) {
+        const int64_t i = ch.start + 4 * (int64_t)j;
+        float g[4];
+        if (f16) {
+          const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(p.grad) + i);
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+          g[0] = a.x; g[1] = a.y; g[2] = b.x; g[3] = b.y;
+        } else {
+          const float4 v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.grad) + i);
+          g[0] = v.x; g[1] = v.y; g[2] = v.z; g[3] = v.w;
+        }
+        float4 m4 = *reinterpret_cast<const float4*>(p.master + i);
+        float m[4] = {m4.x, m4.y, m4.z, m4.w};
+        float mo[4] = {0.f, 0.f, 0.f, 0.f};
+        if (p.momentum) {
+          const float4 o4 = *reinterpret_cast<const float4*>(p.momentum + i);
+          mo[0] = o4.x; mo[1] = o4.y; mo[2] = o4.z; mo[3] = o4.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          g[e] = update_elem(g[e], f16, scaled, factor, m[e], p.momentum ? &mo[e] : nullptr, lr,
+                             momentum, wd);
+        if (p.momentum) *reinterpret_cast<float4*>(p.momentum + i) = make_float4(mo[0], mo[1], mo[2], mo[3]);
+        *reinterpret_cast<float4*>(p.master + i) = make_float4(m[0], m[1], m[2], m[3]);
+        if (f16) {
+          const __half2 d0 = __floats2half2_rn(m[0], m[1]), d1 = __floats2half2_rn(m[2], m[3]);
+          uint2 du;
+          du.x = *reinterpret_cast<const uint32_t*>(&d0);
+          du.y = *reinterpret_cast<const uint32_t*>(&d1);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.data) + i) = du;
+          if (scaled) {
+            const __half2 g0 = __floats2half2_rn(g[0], g[1]), g1 = __floats2half2_rn(g[2], g[3]);
+            uint2 gu;
+            gu.x = *reinterpret_cast<const uint32_t*>(&g0);
+            gu.y = *reinterpret_cast<const uint32_t*>(&g1);
+            *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.grad) + i) = gu;
+          }
+        } else {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.data) + i) =
+              make_float4(m[0], m[1], m[2], m[3]);
+          if (scaled)
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.grad) + i) =
+                make_float4(g[0], g[1], g[2], g[3]);
+        }
+      }
+    } else {
+      for (int32_t j = threadIdx.x; j < ch.len; j += blockDim.x) {
+        const int64_t i = ch.start + j;
+        float m = p.master[i];
+        float mo = p.momentum ? p.momentum[i] : 0.f;
+        const float g = update_elem(load_any(p.grad, p.dtype, i), f16, scaled, factor, m,
+                                    p.momentum ? &mo : nullptr, lr, momentum, wd);
+        if (scaled) store_any(p.grad, p.dtype, i, g);
+        if (p.momentum) p.momentum[i] = mo;
+        p.master[i] = m;
+        store_any(p.data, p.dtype, i, m);
+      }
     }
-    float m = p.master[i];
-    if (wd != 0.f) g = __fadd_rn(g, __fmul_rn(wd, m));
-    float step = __fmul_rn(lr, g);
-    if (p.momentum) {
-      step = __fadd_rn(__fmul_rn(momentum, p.momentum[i]), step);
-      p.momentum[i] = step;
-    }
-    m = __fsub_rn(m, step);
-    p.master[i] = m;
-    store_any(p.data, p.dtype, i, m);
-  });
+  }
 }
 
 __global__ void k_scaler_finish(nnl_scaler_state* s) {
