@@ -1201,6 +1201,47 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // out = q(prev + bias + sum_s partial[s][m][n]), fixed split order; `trans`
 // writes D[m][n] to out[n*ldc + m]
+// the same reduction, 4 consecutive columns per thread (plain layout, N and ldc
+// multiples of 4): float4 partial loads in the same split order, 8 B stores
+__global__ void k_tc_splitk_reduce4(int M, int N, int splits, const float* __restrict__ partial,
+                                    const __half* __restrict__ bias, __half* __restrict__ out,
+                                    int64_t ldc, int acc, int32_t* nonfinite) {
+  int bad = 0;
+  const int64_t total = (int64_t)M * N, total4 = total / 4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total4;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 4 * t;
+    const int64_t m = i / N, n = i % N;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int z = 0; z < splits; ++z) {
+      const float4 p = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + i);
+      s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+    }
+    float v[4] = {s.x, s.y, s.z, s.w};
+    if (bias) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = __fadd_rn(v[e], __half2float(bias[n + e]));
+    }
+    uint2* o = reinterpret_cast<uint2*>(out + m * ldc + n);
+    float p[4] = {0.f, 0.f, 0.f, 0.f};
+    if (acc) {
+      const uint2 u = *o;
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+      p[0] = a.x; p[1] = a.y; p[2] = b.x; p[3] = b.y;
+    }
+    const __half2 h0 = __floats2half2_rn(__fadd_rn(p[0], v[0]), __fadd_rn(p[1], v[1]));
+    const __half2 h1 = __floats2half2_rn(__fadd_rn(p[2], v[2]), __fadd_rn(p[3], v[3]));
+    uint2 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&h0);
+    w.y = *reinterpret_cast<const uint32_t*>(&h1);
+    *o = w;
+    const float2 c0 = __half22float2(h0), c1 = __half22float2(h1);
+    bad |= !isfinite(c0.x) | !isfinite(c0.y) | !isfinite(c1.x) | !isfinite(c1.y);
+  }
+  if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+}
+
 __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __restrict__ partial,
                                    const __half* __restrict__ bias, __half* __restrict__ out,
                                    int64_t ldc, int acc, int trans, int c4, int c4_s2,
@@ -2410,11 +2451,17 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   if (to_partial) {
     const bool mapped = (pl.c4 || pl.s2d) && pb.mode == kWgrad;
     const int c4 = mapped ? g.c : 0;
-    k_tc_splitk_reduce<<<grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st>>>(
-        pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
-        reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, c4,
-        pl.s2d ? pl.s2 : pl.c4_s2, g.r, g.s, pl.s2d && pb.mode == kWgrad ? 1 : 0,
-        pb.nonfinite);
+    if (!mapped && pl.N % 4 == 0 && pl.ldc % 4 == 0 &&
+        !(reinterpret_cast<uintptr_t>(pb.out) & 7))
+      k_tc_splitk_reduce4<<<grid_for((int64_t)pl.M * pl.N / 4, 256), 256, 0, st>>>(
+          pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
+          reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, pb.nonfinite);
+    else
+      k_tc_splitk_reduce<<<grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st>>>(
+          pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
+          reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, c4,
+          pl.s2d ? pl.s2 : pl.c4_s2, g.r, g.s, pl.s2d && pb.mode == kWgrad ? 1 : 0,
+          pb.nonfinite);
     NNL_CHECK_LAUNCH();
   }
   return NNL_OK;
