@@ -235,6 +235,33 @@ __global__ void k_gap_bwd(int64_t n, int64_t hw, int64_t c, const T* __restrict_
   }
 }
 
+// fp16, c % 8 == 0: one thread per (image, 8 channels) computes q(0|prev + dy/hw)
+// once per channel and writes the hw pixels as 16 B stores
+__global__ void k_gap_bwd_h8(int n, int hw, int c, const __half* __restrict__ dy,
+                             __half* __restrict__ dx, int acc) {
+  const int cg = c >> 3;
+  const float fhw = (float)hw;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * cg; t += gridDim.x * blockDim.x) {
+    const int b = t / cg, g = t - b * cg;
+    const uint4 u = *reinterpret_cast<const uint4*>(dy + (int64_t)b * c + g * 8);
+    const __half* h = reinterpret_cast<const __half*>(&u);
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __fdiv_rn(__half2float(h[j]), fhw);
+    uint4* dst = reinterpret_cast<uint4*>(dx + (int64_t)b * hw * c + g * 8);
+    for (int p = 0; p < hw; ++p) {
+      __align__(16) __half o[8];
+      uint4 pv = make_uint4(0, 0, 0, 0);
+      if (acc) pv = dst[(int64_t)p * cg];
+      const __half* ph = reinterpret_cast<const __half*>(&pv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        o[j] = __float2half_rn(__fadd_rn(acc ? __half2float(ph[j]) : 0.f, v[j]));
+      dst[(int64_t)p * cg] = *reinterpret_cast<const uint4*>(o);
+    }
+  }
+}
+
 template <typename T>
 __global__ void k_import(int32_t n, int32_t c, int32_t hw, const float* __restrict__ src,
                          T* __restrict__ dst) {
@@ -468,6 +495,13 @@ int nnl_gap_fwd(int dtype, int64_t n, int64_t hw, int64_t c, const void* x, void
 int nnl_gap_bwd(int dtype, int64_t n, int64_t hw, int64_t c, const void* dy, void* dx,
                 int accumulate, void* stream) {
   if (n * c * hw <= 0) return NNL_OK;
+  if (dtype == NNL_F16 && c % 8 == 0 && n * c < (1ll << 31) &&
+      !((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx)) & 15)) {
+    k_gap_bwd_h8<<<grid_for(n * (c / 8), 256), 256, 0, as_stream(stream)>>>(
+        (int)n, (int)hw, (int)c, (const __half*)dy, (__half*)dx, accumulate);
+    NNL_CHECK_LAUNCH();
+    return NNL_OK;
+  }
   NNL_DISPATCH_DTYPE(dtype, T, {
     k_gap_bwd<T><<<grid_for(n * hw * c, 256), 256, 0, as_stream(stream)>>>(
         n, hw, c, (const T*)dy, (T*)dx, accumulate);
