@@ -348,12 +348,6 @@ __device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr, uint32_t lbo, uin
 }
 
 // instruction descriptor: kind::f16, A/B fp16, D f32, M = 128 (or 256 for a pair)
-// with the matrix base offset (bits 49-51): the row phase (address bits 7-9) of a
-// start address that is not on a 1024 B swizzle-pattern boundary
-__device__ __forceinline__ uint64_t sdesc_sw128_bo(uint32_t saddr, uint32_t lbo, uint32_t sbo,
-                                                   uint32_t bo) {
-  return sdesc_sw128(saddr, lbo, sbo) | ((uint64_t)(bo & 7u) << 49);
-}
 __host__ __device__ constexpr uint32_t idesc_f16(int n, bool a_mn, bool b_mn, int m = 128) {
   return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
