@@ -190,7 +190,9 @@ __device__ __forceinline__ bool red_leader() { return (threadIdx.x >> 3) == 0; }
 
 __device__ __forceinline__ void reduce_partials(const float* __restrict__ partials, int32_t R,
                                                 int32_t c, int ch, double& a, double& b) {
-  __shared__ double sa[kRedLanes][kRedCols + 1], sb[kRedLanes][kRedCols + 1];
+  // fixed order: row lanes -> the 4 lanes of a column inside a warp (xor 8, 16)
+  // -> the 32 warps, serially (was 128 serial steps)
+  __shared__ double sa[kRedLanes / 4][kRedCols + 1], sb[kRedLanes / 4][kRedCols + 1];
   const int col = threadIdx.x & 7, lane = threadIdx.x >> 3;
   double x = 0.0, y = 0.0;
   if (ch < c) {
@@ -199,13 +201,20 @@ __device__ __forceinline__ void reduce_partials(const float* __restrict__ partia
       y += (double)partials[(int64_t)r * 2 * c + c + ch];
     }
   }
-  sa[lane][col] = x;
-  sb[lane][col] = y;
+  x += __shfl_xor_sync(0xffffffffu, x, 8);
+  y += __shfl_xor_sync(0xffffffffu, y, 8);
+  x += __shfl_xor_sync(0xffffffffu, x, 16);
+  y += __shfl_xor_sync(0xffffffffu, y, 16);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) < 8) {
+    sa[w][col] = x;
+    sb[w][col] = y;
+  }
   __syncthreads();
   a = 0.0;
   b = 0.0;
   if (lane == 0) {
-    for (int l = 0; l < kRedLanes; ++l) {
+    for (int l = 0; l < kRedLanes / 4; ++l) {
       a += sa[l][col];
       b += sb[l][col];
     }

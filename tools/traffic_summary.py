@@ -37,6 +37,8 @@ def main():
     step = seq[ends[-2] + 1:ends[-1] + 1] if len(ends) >= 2 else seq
     fam = collections.defaultdict(lambda: {"launches": 0, "ms": 0.0, "dram_bytes": 0.0})
     for d in step:
+        if "nnl::" not in d["name"]:
+            continue  # e.g. bench.py's GPU-lead spins around profiled nodes
         k = re.sub(r"\(.*", "", d["name"]).replace("void ", "")
         k = re.sub(r"<.*", "", k)
         f = fam[k]
