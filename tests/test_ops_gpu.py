@@ -276,3 +276,25 @@ def test_bn_residual_tail(nnl, half, c, shared):
                       (runs[0][4], ob.grad)):
         scale = np.abs(want).max() + 1e-6
         assert np.abs(np.asarray(got, np.float64) - want).max() / scale < (2e-2 if half else 1e-4)
+
+
+def test_maxpool_backward_accumulates(nnl):
+    """R2 on the 3x3/s2/p1 pool backward: a second contribution lands as
+    q(prev + scatter), with prev the first contribution's stored bits."""
+    import paper_2102_06725_b200.functions as F
+    _ctx(nnl, True)
+    rng = np.random.default_rng(8)
+    x = (np.round(rng.uniform(-2, 2, (2, 16, 14, 14)) * 4) / 4).astype(np.float32)
+    v = nnl.Variable(x.shape, need_grad=True)
+    v.d = x
+    y = F.max_pooling(v, (3, 3), (2, 2), pad=(1, 1))
+    y.forward()
+    y.backward(1.0)
+    _, arg = O.maxpool_forward(O.q16(x), (3, 3), (2, 2), (1, 1))
+    gy = O.q16(rng.uniform(-1, 1, y.shape).astype(np.float32))
+    y.g = gy
+    prev = O.q16(rng.uniform(-1, 1, x.shape).astype(np.float32))
+    v.g = prev
+    y.parent.impl.backward(y.parent, [y.grad], [v.grad], [True])
+    scat = O.maxpool_backward(gy, arg, x.shape, (3, 3), (2, 2), (1, 1))
+    close(v.g, O.q16(prev + scat), 0, 0)
