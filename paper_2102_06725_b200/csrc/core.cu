@@ -262,6 +262,21 @@ __global__ void k_gap_bwd_h8(int n, int hw, int c, const __half* __restrict__ dy
   }
 }
 
+// narrow-channel NCHW f32 -> NHWC (the network input, c = 3): one thread per
+// pixel reads its c channel planes (coalesced across threads) and writes the c
+// contiguous elements
+template <typename T>
+__global__ void k_import_narrow(int32_t n, int32_t c, int32_t hw, const float* __restrict__ src,
+                                T* __restrict__ dst) {
+  const int total = n * hw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int b = i / hw, pix = i - b * hw;
+    const float* s = src + (int64_t)b * c * hw + pix;
+    T* d = dst + (int64_t)i * c;
+    for (int ch = 0; ch < c; ++ch) Elem<T>::store(d + ch, __ldg(s + (int64_t)ch * hw));
+  }
+}
+
 template <typename T>
 __global__ void k_import(int32_t n, int32_t c, int32_t hw, const float* __restrict__ src,
                          T* __restrict__ dst) {
@@ -516,7 +531,11 @@ int nnl_import_f32(int dtype, int32_t n, int32_t c, int32_t hw, const float* src
   if (total <= 0) return NNL_OK;
   if (total >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "import of >= 2^31 elements");
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_import<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(n, c, hw, src, (T*)dst);
+    if (c <= 4 && hw > 1)
+      k_import_narrow<T><<<grid_for((int64_t)n * hw, 256), 256, 0, as_stream(stream)>>>(
+          n, c, hw, src, (T*)dst);
+    else
+      k_import<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(n, c, hw, src, (T*)dst);
   });
   NNL_CHECK_LAUNCH();
   return NNL_OK;
