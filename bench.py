@@ -1,7 +1,12 @@
 #!/usr/bin/env python
-"""ResNet-50 mixed-precision training throughput on B200 (BASELINE.json metric).
+"""Training-step throughput on B200 for the BASELINE.json configs.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config resnet50|resnet18|lenet|mlp]
+
+The default (what the driver runs) is C4: ResNet-50 mixed precision, batch
+256 per GPU -- the BASELINE.json metric.  `--config` gives the C1-C3 lines
+(MLP and LeNet are latency configs reported in us/step).
 
 One process per GPU (torchrun for N>1; NCCL all-reduce of gradients).  Our
 arm prints ONE JSON line on rank 0:
@@ -35,9 +40,49 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ResNet-50 mixed-precision train images/sec at 1/2/4/8 B200; % of roofline"
 UNIT = "img/s"
-PER_GPU_BATCH = 256
-IMAGE = 224
-CLASSES = 1000
+
+
+# BASELINE.json configs[0..3]; C4 (resnet50) is the headline line the driver runs,
+# the others are `--config` lines (C5, the all-reduce sweep, is tools/allreduce_sweep.py)
+CONFIGS = {
+    "mlp": dict(
+        metric="MLP 784-256-10 fp32 train step (fwd+bwd+Momentum SGD), batch 64: us/step",
+        unit="us/step", higher_is_better=False, batch=64, shape=(784,), classes=10,
+        half=False, scaler=None, lr=0.1, momentum=0.9, wd=0.0,
+        workload="C1 MLP 784-256-10 (ReLU, softmax CE), fp32, momentum SGD 0.9, lr 0.1"),
+    "lenet": dict(
+        metric="LeNet 28x28 fp16 + dynamic loss scaling train step, batch 128: us/step",
+        unit="us/step", higher_is_better=False, batch=128, shape=(1, 28, 28), classes=10,
+        half=True, scaler=(8.0, 2.0, 2000), lr=0.01, momentum=0.0, wd=0.0,
+        workload="C2 LeNet (conv5-pool2-relu x2, affine50-relu, affine10), fp16 storage + "
+                 "dynamic loss scaling (8, x2, 2000), SGD lr 0.01"),
+    "resnet18": dict(
+        metric="ResNet-18 CIFAR-10 shape mixed-precision train images/sec (32x32, batch 128/GPU)",
+        unit="img/s", higher_is_better=True, batch=128, shape=(3, 32, 32), classes=10,
+        half=True, scaler=(8.0, 2.0, 2000), lr=0.1, momentum=0.9, wd=1e-4,
+        workload="C3 ResNet-18 CIFAR (3x3 stem, [2,2,2,2] basic blocks), fp16 storage + dynamic "
+                 "loss scaling (8, x2, 2000), momentum SGD 0.9, wd 1e-4, lr 0.1"),
+    "resnet50": dict(
+        metric=METRIC, unit=UNIT, higher_is_better=True, batch=256, shape=(3, 224, 224),
+        classes=1000, half=True, scaler=(8.0, 2.0, 2000), lr=0.1, momentum=0.9, wd=1e-4,
+        workload="ResNet-50 v1.5 224x224 train step: fp16 storage + dynamic loss scaling "
+                 "(8, x2, 2000), momentum SGD 0.9, wd 1e-4, lr 0.1"),
+}
+
+
+def build_graph(nn, F, networks, name, bs):
+    cf = CONFIGS[name]
+    xv = nn.Variable((bs,) + cf["shape"])
+    tv = nn.Variable((bs,))
+    if name == "mlp":
+        logits = networks.mlp(xv, 10, hidden=(256,))
+    elif name == "lenet":
+        logits = networks.lenet(xv, 10)
+    elif name == "resnet18":
+        logits = networks.resnet18_cifar(xv, 10)
+    else:
+        logits = networks.resnet50(xv, cf["classes"])
+    return {"x": xv, "label": tv, "loss": F.softmax_cross_entropy(logits, tv)}
 
 
 def parse():
@@ -46,7 +91,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="per-GPU batch")
+    ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (0: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager steps (no CUDA graph)")
@@ -127,40 +173,72 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def oracle_resnet50_rate(batch: int, steps: int, warmup: int) -> tuple[float, int]:
-    """img/s of the oracle port (numpy) of the reference training step."""
+def _oracle_builder(name):
+    from oracle import nnl_oracle as O
+    if name == "mlp":
+        return lambda m, a, t: m.sce(O.mlp(m, a, 10, hidden=(256,)), t)
+    if name == "lenet":
+        return lambda m, a, t: m.sce(O.lenet(m, a, 10), t)
+    if name == "resnet18":
+        return lambda m, a, t: m.sce(O.resnet18_cifar(m, a, 10), t)
+    return lambda m, a, t: m.sce(O.resnet50(m, a, CONFIGS["resnet50"]["classes"]), t)
+
+
+# bounded CPU samples: images per oracle step (full batch where it takes < ~1 s)
+CPU_SAMPLE = {"mlp": 64, "lenet": 128, "resnet18": 8, "resnet50": 1}
+
+
+def oracle_rate(name: str, batch: int, steps: int, warmup: int) -> tuple[float, int, float]:
+    """(img/s, host threads, s/step) of the oracle port (numpy) of the reference
+    training step for config `name` on `batch` images."""
     import numpy as np
     from oracle import nnl_oracle as O
-    x = O.uniform(1, 0, (batch, 3, IMAGE, IMAGE), 0.0, 1.0)
-    lab = (np.arange(batch) % CLASSES).astype(np.float32)
-    tr = O.Trainer(lambda m, a, t: m.sce(O.resnet50(m, a, CLASSES), t), 1, batch, 0.1, seed=0,
-                   half=True, scaler=O.Scaler(8.0, 2.0, 2000), momentum=0.9,
-                   weight_decay=1e-4)
+    cf = CONFIGS[name]
+    x = O.uniform(1, 0, (batch,) + cf["shape"], 0.0, 1.0)
+    lab = (np.arange(batch) % cf["classes"]).astype(np.float32)
+    sc = O.Scaler(*cf["scaler"]) if cf["scaler"] else None
+    tr = O.Trainer(_oracle_builder(name), 1, batch, cf["lr"], seed=0, half=cf["half"],
+                   scaler=sc, momentum=cf["momentum"], weight_decay=cf["wd"])
     for _ in range(warmup):
         tr.step(x, lab)
     t0 = time.perf_counter()
     for _ in range(steps):
         tr.step(x, lab)
-    dt = time.perf_counter() - t0
-    return batch * steps / dt, len(os.sched_getaffinity(0))
+    dt = (time.perf_counter() - t0) / steps
+    return batch / dt, len(os.sched_getaffinity(0)), dt
+
+
+def _rate_value(name: str, img_s: float, batch: int) -> float:
+    """The config's metric from an images/sec rate (us/step at `batch` for the
+    latency configs)."""
+    if CONFIGS[name]["unit"] == "us/step":
+        return 1e6 * batch / img_s
+    return img_s
 
 
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
+    name = args.config
+    cf = CONFIGS[name]
     steps, warmup = max(1, args.steps), max(0, args.warmup)
-    rate, cores = oracle_resnet50_rate(1, steps, warmup)
+    sample = CPU_SAMPLE[name]
+    if cf["unit"] == "us/step":  # the reference path on the full per-GPU batch
+        sample = args.batch or cf["batch"]
+    rate, cores, sps = oracle_rate(name, sample, steps, warmup)
+    value = _rate_value(name, rate, sample)
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(rate, 4), "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": warmup, "ms_per_step": round(1000.0 / rate, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16-storage/f32",
+        "impl": "reference", "metric": cf["metric"], "value": round(value, 4), "unit": cf["unit"],
+        "n_gpus": args.gpus, "steps": steps, "warmup": warmup, "ms_per_step": round(1000 * sps, 2),
+        "higher_is_better": cf["higher_is_better"], "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16-storage/f32" if cf["half"] else "f32",
         "data": "synthetic (RngState seed 1)",
-        "config": {"workload": "ResNet-50 v1.5 224x224 train step, fp16 storage + dynamic loss "
-                               "scaling, momentum SGD (oracle port of the reference path)",
-                   "sample": "1 image per step", "parallelism": "host threads"},
-        "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": "ResNet-50 train step on 1 image (oracle/nnl_oracle.py)"},
-        "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+        "config": {"workload": cf["workload"] + " (oracle port of the reference path)",
+                   "sample": f"{sample} image(s) per step", "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(value, 4), "unit": cf["unit"], "cores": cores,
+                         "kind": "port",
+                         "sample": f"{name} train step on {sample} image(s) (oracle/nnl_oracle.py)"},
+        "e2e": {"value": round(value, 4), "unit": cf["unit"], "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -189,26 +267,24 @@ def main():
     from paper_2102_06725_b200.communicator import DataParallelTrainer
     from paper_2102_06725_b200.profiler import PROFILER
 
-    B = args.batch
-    nn.set_default_context(nn.ExecutionContext(type_config=nn.TypeConfig.HALF))
-
-    def build(bs):
-        xv = nn.Variable((bs, 3, IMAGE, IMAGE))
-        tv = nn.Variable((bs,))
-        loss = F.softmax_cross_entropy(networks.resnet50(xv, CLASSES), tv)
-        return {"x": xv, "label": tv, "loss": loss}
-
-    trainer = DataParallelTrainer(world, B * world, build, lr=0.1, seed=0,
-                                  loss_scaling=nn.DynamicLossScaler(8.0, 2.0, 2000),
-                                  check_sync=False, momentum=0.9, weight_decay=1e-4)
+    name = args.config
+    cf = CONFIGS[name]
+    B = args.batch or cf["batch"]
+    nn.set_default_context(nn.ExecutionContext(
+        type_config=nn.TypeConfig.HALF if cf["half"] else nn.TypeConfig.FLOAT))
+    scaler = nn.DynamicLossScaler(*cf["scaler"]) if cf["scaler"] else None
+    trainer = DataParallelTrainer(world, B * world, lambda bs: build_graph(nn, F, networks, name, bs),
+                                  lr=cf["lr"], seed=0, loss_scaling=scaler, check_sync=False,
+                                  momentum=cf["momentum"], weight_decay=cf["wd"])
     # this rank's shard of the global synthetic batch: counter offset = shard start
-    rng = nn.RngState(1, counter=rank * B * 3 * IMAGE * IMAGE)
-    xdev = rng.next_uniform_device((B, 3, IMAGE, IMAGE), 0.0, 1.0)
+    per_img = int(np.prod(cf["shape"]))
+    rng = nn.RngState(1, counter=rank * B * per_img)
+    xdev = rng.next_uniform_device((B,) + cf["shape"], 0.0, 1.0)
     x_host = torch.empty(xdev.shape, dtype=torch.float32).pin_memory()
     x_host.copy_(xdev)
     del xdev
     lab_host = torch.empty(B, dtype=torch.float32).pin_memory()
-    lab_host.copy_(torch.from_numpy(((np.arange(B) + rank * B) % CLASSES).astype(np.float32)))
+    lab_host.copy_(torch.from_numpy(((np.arange(B) + rank * B) % cf["classes"]).astype(np.float32)))
     xs, ls = x_host.numpy(), lab_host.numpy()
 
     def e2e_step():
@@ -252,7 +328,7 @@ def main():
     host_ms = (time.perf_counter() - t0) * 1000.0
     sync()
     graph = False
-    if world == 1 and not args.no_graph:
+    if not args.no_graph:
         try:
             trainer.capture_graph()
             graph = True
@@ -277,7 +353,8 @@ def main():
     launches = int(_lib.lib().nnl_launch_count(1))
     if graph:  # replays issue no host launches: count the recorded libnnl kernels
         launches = trainer.graph_kernels * K
-    value = B * world * K / (ms / 1000.0)
+    img_s = B * world * K / (ms / 1000.0)
+    value = ms * 1000.0 / K if cf["unit"] == "us/step" else img_s
 
     # ---- end-to-end through the public API (H2D from pinned memory + loss D2H) ----
     sync()
@@ -288,9 +365,9 @@ def main():
     e2.record()
     sync()
     ms_e2e = max_over_ranks(max(s2.elapsed_time(e2), (time.perf_counter() - w0) * 1000.0))
-    e2e = B * world * K / (ms_e2e / 1000.0)
+    e2e = ms_e2e * 1000.0 / K if cf["unit"] == "us/step" else B * world * K / (ms_e2e / 1000.0)
 
-    # ---- roofline of the tcgen05 GEMM kernels from one profiled (eager) step ----
+    # ---- roofline of the GEMM kernels from one profiled (eager) step ----
     saved_graph = getattr(trainer, "_graph", None)
     trainer._graph = None
     PROFILER.reset()
@@ -305,7 +382,7 @@ def main():
     gemm_fl = sum(v["flops"] for k, v in prof.items())
     total_ms = sum(v["ms"] for v in prof.values())
     pk = peaks()
-    traffic = gemm_traffic()
+    traffic = gemm_traffic() if name == "resnet50" else None
     achieved = gemm_fl / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
 
@@ -316,39 +393,50 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rate, cores = oracle_resnet50_rate(1, 2, 0)
-        cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": "oracle ResNet-50 fp16-storage train step, 1 image x 2 steps"}
+        sample = CPU_SAMPLE[name]
+        reps = 2 if name in ("resnet18", "resnet50") else 20
+        rate, cores, _ = oracle_rate(name, sample, reps, 1 if reps > 2 else 0)
+        cpu = {"value": round(_rate_value(name, rate, sample), 4), "unit": cf["unit"],
+               "cores": cores, "kind": "port",
+               "sample": f"oracle {name} train step, {sample} image(s) x {reps} steps"}
 
     h2d = int(x_host.numel() * 4 + lab_host.numel() * 4)
+    latency = cf["unit"] == "us/step"
     line = {
-        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": round(ms / K, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "metric": cf["metric"], "value": round(value, 2), "unit": cf["unit"], "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
+        "higher_is_better": cf["higher_is_better"],
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16" if cf["half"] else "f32",
         "data": "synthetic (RngState seed 1, uniform [0,1)), random-init weights (registry seed 0)",
-        "config": {"workload": "ResNet-50 v1.5 224x224 train step: fp16 storage + dynamic loss "
-                               "scaling (8, x2, 2000), momentum SGD 0.9, wd 1e-4, lr 0.1",
-                   "global_batch": B * world, "per_gpu_batch": B, "image": IMAGE,
+        "config": {"workload": cf["workload"], "name": name,
+                   "global_batch": B * world, "per_gpu_batch": B, "input": list(cf["shape"]),
                    "parallelism": f"dp{world}", "cuda_graph": graph,
-                   "host_ms_per_eager_step": round(host_ms, 2),
-                   "l2": "inputs+activations (~20 GB/step) far exceed the 126 MB L2"},
-        "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "host_ms_per_eager_step": round(host_ms, 3),
+                   "l2": ("inputs+activations (~20 GB/step) far exceed the 126 MB L2"
+                          if name == "resnet50" else
+                          "working set fits in L2: steps run L2-warm (no flush)")},
+        "e2e": {"value": round(e2e, 2), "unit": cf["unit"], "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4,
                 "api": "DataParallelTrainer.step_async (H2D of step i+1 overlaps step i)"
                        if world == 1 else "DataParallelTrainer.step"},
         "gpu_launches": launches,
-        "roofline": {"bound": "tensor", "kernel": "k_tc_gemm (conv/affine fwd+dgrad+wgrad)",
-                     "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": "tensor", "kernel": "GEMM kernels (conv/affine fwd+dgrad+wgrad)",
+                     "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4) if peak else None,
                      "traffic": (traffic or {}).get("bytes_per_step"), "traffic_detail": traffic,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "gemm_share_of_step": round(gemm_ms / total_ms, 3) if total_ms else None,
-                     "gemm_tflop_per_step": round(gemm_fl / 1e12, 3)},
+                     "gemm_tflop_per_step": round(gemm_fl / 1e12, 4)},
         "clocks": clk.summary(),
         "last_loss": loss,
         "profile_ms": {k: round(v["ms"], 3) for k, v in sorted(prof.items(),
                                                                 key=lambda kv: -kv[1]["ms"])},
     }
+    if latency:
+        line["roofline"]["note"] = ("launch-latency bound: us/step (CUDA graph replay of "
+                                    f"{trainer.graph_kernels if graph else '?'} kernels) is the "
+                                    "figure of merit; the tensor fraction is informative only")
+        line["images_per_s"] = round(img_s, 1)
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)

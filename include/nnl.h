@@ -121,10 +121,12 @@ int nnl_affine_bwd_weight(int dtype, int64_t batch, int64_t in_f, int64_t in_c, 
 
 /* ---- Convolution: functions.py:152-214 ---------------------------------- */
 size_t nnl_conv2d_workspace_size(const nnl_conv_shape* cs, int dtype, int pass);
-/* y = conv(x, w) + b.  stat_partials (nullable, f32 [ceil(M/128)][2][K]) receives
-   per-row-tile sum / sum of squares of the ROUNDED outputs for a following BN. */
+/* y = conv(x, w) + b.  stat_partials (nullable, f32 [nnl_conv2d_stat_rows][2][K])
+   receives per-CTA sums of (y - K) and (y - K)^2 over the ROUNDED outputs for a
+   following BN, K = stat_shift[k] (nullable: 0) -- the BN's centre, so that a
+   channel with |mean| >> std keeps its variance (nnl_bn_fwd_train `shift`). */
 int nnl_conv2d_fwd(const nnl_conv_shape* cs, int dtype, const void* x, const void* w,
-                   const void* b, void* y, float* stat_partials,
+                   const void* b, void* y, float* stat_partials, const float* stat_shift,
                    void* ws, size_t ws_bytes, void* stream);
 int nnl_conv2d_bwd_data(const nnl_conv_shape* cs, int dtype, const void* dy, const void* w,
                         void* dx, int accumulate, void* ws, size_t ws_bytes, void* stream);
@@ -201,14 +203,19 @@ int nnl_sce_bwd(int dtype, int64_t batch, int64_t classes, const void* logits,
 /* ---- BatchNormalization: functions.py:363-441 --------------------------- */
 size_t nnl_bn_workspace_size(int64_t rows, int32_t c);
 /* rows = N*H*W (channel-innermost).  stat_partials (nullable) are the conv
-   epilogue partials; save_mean/save_istd (f32 [c]) feed backward.
+   epilogue partials, centred on shift[c]; without them the statistics pass
+   centres on x's first row.  mean = K + sum(x-K)/n, var = sum((x-K)^2)/n -
+   (sum(x-K)/n)^2 in f64 (the reference's two-pass np.var, functions.py:402,
+   without its cancellation).  shift (nullable, f32 [c], in/out) receives the
+   batch mean: the centre of the next call.  save_mean/save_istd (f32 [c])
+   feed backward.
    residual (nullable): the residual tail BN -> Add2 -> [ReLU] in one pass,
    y = [relu](q(q(BN(x)) + residual)) -- each step rounded exactly as the
    separate functions would (functions.py:412-416, then Add2, then ReLU). */
 int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x,
                      const float* gamma, const float* beta,
                      float* running_mean, float* running_var, float eps, float momentum,
-                     const float* stat_partials, int32_t n_partials,
+                     const float* stat_partials, int32_t n_partials, float* shift,
                      float* save_mean, float* save_istd, void* y, const void* residual,
                      int fuse_relu, void* ws, size_t ws_bytes, void* stream);
 int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x,
@@ -300,6 +307,38 @@ int nnl_bucket_pack(const nnl_param_slot* slots, const nnl_chunk* chunks, const 
 int nnl_bucket_unpack_mean(const nnl_param_slot* slots, const nnl_chunk* chunks,
                            const int64_t* chunk_pos, int32_t n_chunks, const float* bucket,
                            int32_t world, int32_t* nonfinite, void* stream);
+
+/* ---- Communicator: communicator.py:69-105 ---------------
+ * One rank per process/GPU over NCCL (resolved at run time from the process's
+ * libnccl).  nnl_comm_allreduce_mean is the whole bucket exchange of
+ * Communicator.all_reduce(buffers, division) on the caller's stream: pack the
+ * gradients into the f32 bucket, exchange, unpack grad = q(sum / f32(W))
+ * (division) or q(sum), OR-ing non-finite results into *nonfinite.
+ *   NNL_COMM_NCCL : ncclAllReduce(sum) (NCCL's ring / NVLS summation order)
+ *   NNL_COMM_EXACT: the reference's fold acc = ((b0 + b1) + b2) + ... in
+ *                   ascending rank order (R9, communicator.py:99-103), bit-exact,
+ *                   with the bytes of a ring all-reduce: send/recv of each
+ *                   rank's 1/W slice, fold, in-place all-gather.  Its bucket
+ *                   holds nnl_comm_bucket_elems(n) elements and it needs
+ *                   nnl_comm_workspace_size(n) bytes of workspace.
+ * Errors: CollectiveTimeout for NCCL system/remote failures.  Stream-ordered
+ * and CUDA-graph capturable. */
+#define NNL_COMM_NCCL 0
+#define NNL_COMM_EXACT 1
+#define NNL_COMM_ID_BYTES 128
+typedef struct nnl_comm nnl_comm;
+int nnl_comm_unique_id(void* id_out /* NNL_COMM_ID_BYTES */);
+int nnl_comm_init(nnl_comm** out, int32_t world, int32_t rank, const void* unique_id,
+                  int32_t mode);
+int nnl_comm_destroy(nnl_comm* comm);
+int64_t nnl_comm_bucket_elems(const nnl_comm* comm, int64_t n);
+size_t nnl_comm_workspace_size(const nnl_comm* comm, int64_t n);
+int nnl_comm_allreduce_mean(nnl_comm* comm, const nnl_param_slot* slots, const nnl_chunk* chunks,
+                            const int64_t* chunk_pos, int32_t n_chunks, float* bucket, int64_t n,
+                            int32_t divide, int32_t* nonfinite, void* ws, size_t ws_bytes,
+                            void* stream);
+/* plain in-place f32 sum over the ranks (e.g. the step's loss) */
+int nnl_comm_allreduce_sum_f32(nnl_comm* comm, float* buf, int64_t n, void* stream);
 
 /* ---- API-boundary marshaling (Variable.d get/set, graph.py:137-155) ------
  * import: f32 NCHW (logical, host order) -> dtype NHWC storage, quantizing;

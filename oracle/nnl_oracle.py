@@ -560,11 +560,13 @@ class Sgd:
     Masters are taken lazily on first use; parameters do not change before
     the first update, so this equals setup()-time copies (R11)."""
 
-    def __init__(self, model: "Model", lr: float, momentum=0.0, weight_decay=0.0):
+    def __init__(self, model: "Model", lr: float, momentum=0.0, weight_decay=0.0,
+                 clip_norm=None):
         self.model = model
         self.lr = lr
         self.momentum = momentum
         self.wd = weight_decay
+        self.clip_norm = clip_norm
         self.master: dict[str, np.ndarray] = {}
         self.vel: dict[str, np.ndarray] = {}
 
@@ -581,6 +583,16 @@ class Sgd:
     def scale_grad(self, factor: float):
         for v in self.params.values():
             v.grad = store(v.grad * F32(factor), v.half)                          # R10
+
+    def clip_grad_by_norm(self):
+        """solver.py:119-129: per-parameter f32 sums of squares, summed as Python
+        floats, f32 sqrt; scale by clip/total only when total exceeds clip."""
+        if self.clip_norm is None:
+            return
+        total = np.sqrt(F32(sum(float(np.sum(np.square(v.grad, dtype=F32)))
+                                for v in self.params.values())))
+        if total > self.clip_norm:
+            self.scale_grad(self.clip_norm / float(total))
 
     def update(self):
         lr = F32(self.lr)
@@ -607,6 +619,7 @@ def dynamic_step(sc: Scaler, opt: Sgd) -> bool:
         sc.counter = 0
         return False
     opt.scale_grad(1.0 / sc.loss_scale)
+    opt.clip_grad_by_norm()
     opt.update()
     if sc.counter > sc.interval:
         sc.loss_scale *= sc.factor

@@ -94,7 +94,7 @@ _SIGS = {
                                         C.c_int, p, p, sz, p]),
     "nnl_conv2d_workspace_size": (sz, [p, C.c_int, C.c_int]),
     "nnl_conv2d_stat_rows": (i32, [p, C.c_int]),
-    "nnl_conv2d_fwd": (C.c_int, [p, C.c_int, p, p, p, p, p, p, sz, p]),
+    "nnl_conv2d_fwd": (C.c_int, [p, C.c_int, p, p, p, p, p, p, p, sz, p]),
     "nnl_conv2d_bwd_data": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, sz, p]),
     "nnl_conv2d_bwd_weight": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, C.c_int, p, p, sz, p]),
     "nnl_conv2d_bwd_data_bn_rows": (i32, [p, C.c_int]),
@@ -110,7 +110,7 @@ _SIGS = {
     "nnl_sce_bwd": (C.c_int, [C.c_int, i64, i64, p, p, p, p, p, C.c_int, p]),
     "nnl_bn_workspace_size": (sz, [i64, i32]),
     "nnl_bn_fwd_train": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, f32, f32, p, i32, p, p, p,
-                                   p, C.c_int, p, sz, p]),
+                                   p, p, C.c_int, p, sz, p]),
     "nnl_bn_fwd_eval": (C.c_int, [C.c_int, i64, i32, p, p, p, p, p, f32, p, p, p, p, C.c_int,
                                   p]),
     "nnl_bn_bwd": (C.c_int, [C.c_int, i64, i32, p, p, C.c_int, p, p, C.c_int, p, p, p, p,
@@ -126,6 +126,13 @@ _SIGS = {
     "nnl_bucket_pack": (C.c_int, [p, p, p, i32, p, p]),
     "nnl_bucket_unpack_mean": (C.c_int, [p, p, p, i32, p, i32, p, p]),
     "nnl_fold_f32": (C.c_int, [i32, p, i64, p, p]),
+    "nnl_comm_unique_id": (C.c_int, [p]),
+    "nnl_comm_init": (C.c_int, [C.POINTER(p), i32, i32, p, i32]),
+    "nnl_comm_destroy": (C.c_int, [p]),
+    "nnl_comm_bucket_elems": (i64, [p, i64]),
+    "nnl_comm_workspace_size": (sz, [p, i64]),
+    "nnl_comm_allreduce_mean": (C.c_int, [p, p, p, p, i32, p, i64, i32, p, p, sz, p]),
+    "nnl_comm_allreduce_sum_f32": (C.c_int, [p, p, i64, p]),
     "nnl_import_f32": (C.c_int, [C.c_int, i32, i32, i32, p, p, p]),
     "nnl_export_f32": (C.c_int, [C.c_int, i32, i32, i32, p, p, p]),
 }

@@ -141,8 +141,21 @@ def load(path: str, params: dict, solver=None, scaler=None) -> None:
         for name, slot in solver.slots.items():
             shape = tuple(slot.param.shape)
             for key, dst in ((MASTER + name, slot.master), (MOMENTUM + name, slot.velocity)):
-                if dst is None or key not in recs:
+                if dst is None:
                     continue
+                if key not in recs:
+                    # a params-only file (e.g. the reference's parameter.bin): the
+                    # master restarts from the loaded weight (R11, solver.py:89-92)
+                    # and the velocity from zero, as a fresh setup() would
+                    if key.startswith(MASTER):
+                        p = slot.param.data
+                        _lib.call("nnl_export_f32", p.code, 1, 1, p.size, p.ptr,
+                                  dst.data_ptr(), _lib.stream())
+                    else:
+                        dst.zero_()
+                    continue
+                if tuple(recs[key].shape) != shape:
+                    raise ShapeMismatch(f"{key}: checkpoint shape {recs[key].shape} != {shape}")
                 src = t.from_numpy(_logical_to_physical(recs[key].values, shape).reshape(-1))
                 dst.copy_(src.to(dst.device))
     if scaler is not None and SCALER in recs:

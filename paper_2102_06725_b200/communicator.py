@@ -20,6 +20,7 @@ division)``, ``barrier``, ``rank``, ``n_workers``):
 
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
 import threading
 from dataclasses import dataclass, field
@@ -66,9 +67,11 @@ def bucket_layout(sizes: list[int]) -> list[int]:
 
 
 class BucketPlan:
-    """Packing of a list of gradient NdArrays into one f32 device bucket."""
+    """Packing of a list of gradient NdArrays into one f32 device bucket
+    (``pad_to``: bucket elements, >= the packed total; the exact all-reduce
+    needs a multiple of the world size)."""
 
-    def __init__(self, arrays: list[NdArray], slot_base=None):
+    def __init__(self, arrays: list[NdArray], slot_base=None, pad_to: int = 0):
         t = _lib.torch()
         self.arrays = list(arrays)
         self.total = sum(a.size for a in arrays)
@@ -83,12 +86,16 @@ class BucketPlan:
         self._pos = t.from_numpy(pos).to(_lib.device()) if len(pos) else \
             t.zeros(1, dtype=t.int64, device=_lib.device())
         self.n_chunks = len(chunks)
-        self.bucket = t.empty(max(self.total, 1), dtype=t.float32, device=_lib.device())
+        self.bucket = t.empty(max(self.total, pad_to, 1), dtype=t.float32, device=_lib.device())
         self.signature = tuple((a.shape, a.dtype.value) for a in arrays)
 
     def pack(self, stream: int) -> None:
         _lib.call("nnl_bucket_pack", self._slots.data_ptr(), self._chunks.data_ptr(),
                   self._pos.data_ptr(), self.n_chunks, self.bucket.data_ptr(), stream)
+
+    def tables(self):
+        return (self._slots.data_ptr(), self._chunks.data_ptr(), self._pos.data_ptr(),
+                self.n_chunks)
 
     def unpack_mean(self, src_ptr: int, world: int, nonfinite_ptr, stream: int) -> None:
         _lib.call("nnl_bucket_unpack_mean", self._slots.data_ptr(), self._chunks.data_ptr(),
@@ -216,12 +223,79 @@ class CommunicatorGroup:
 
 
 # ---------------------------------------------------------------------------
-# multi-process NCCL transport
+# multi-process transport: libnnl's NCCL communicator (nnl_comm_*)
+
+COMM_MODES = {"nccl": 0, "exact": 1}
+
+
+class NcclComm:
+    """Owner of one ``nnl_comm`` handle (include/nnl.h): NCCL over NVLink,
+    driven entirely from libnnl on the caller's stream.  torch.distributed is
+    only the rendezvous: it broadcasts rank 0's ncclUniqueId."""
+
+    def __init__(self, dist, group, rank: int, world: int, mode: str):
+        t = _lib.torch()
+        self.mode = mode
+        idbuf = t.zeros(128, dtype=t.uint8, device=_lib.device())
+        if rank == 0:
+            raw = (C.c_uint8 * 128)()
+            _lib.call("nnl_comm_unique_id", raw)
+            idbuf.copy_(t.frombuffer(bytearray(bytes(raw)), dtype=t.uint8))
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast(idbuf, src=src, group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(bytes(idbuf.cpu().numpy()))
+        handle = C.c_void_p()
+        _lib.call("nnl_comm_init", C.byref(handle), world, rank, uid, COMM_MODES[mode])
+        self.handle = handle
+
+    def bucket_elems(self, n: int) -> int:
+        return int(_lib.lib().nnl_comm_bucket_elems(self.handle, n))
+
+    def allreduce_mean(self, plan: "BucketPlan", divide: bool, nonfinite_ptr, stream: int,
+                       ws=None) -> None:
+        nbytes = int(_lib.lib().nnl_comm_workspace_size(self.handle, plan.total))
+        wp = ws.data_ptr() if ws is not None else None
+        if nbytes and (ws is None or ws.numel() < nbytes):
+            raise ValueError("exact all-reduce workspace too small")
+        _lib.call("nnl_comm_allreduce_mean", self.handle, *plan.tables(), plan.bucket.data_ptr(),
+                  plan.total, 1 if divide else 0, nonfinite_ptr, wp, nbytes, stream)
+        for a in plan.arrays:
+            a.mark_set()
+
+    def allreduce_sum_f32(self, tensor, stream: int) -> None:
+        _lib.call("nnl_comm_allreduce_sum_f32", self.handle, tensor.data_ptr(), tensor.numel(),
+                  stream)
+
+    def workspace(self, n: int):
+        nbytes = int(_lib.lib().nnl_comm_workspace_size(self.handle, n))
+        if not nbytes:
+            return None
+        t = _lib.torch()
+        return t.empty(nbytes, dtype=t.uint8, device=_lib.device())
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().nnl_comm_destroy(h)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+            self.handle = None
+
 
 class DataParallelCommunicator:
-    """One rank per process; NCCL over NVLink through torch.distributed."""
+    """One rank per process (paper Listing 3, MultiProcessDataParalellCommunicator).
 
-    def __init__(self, group=None, bucket_bytes: int = 32 << 20):
+    Over an NCCL process group the exchange is libnnl's communicator
+    (``NcclComm``: pack + ncclAllReduce / rank-ordered exact fold + unpack in
+    one C call, CUDA-graph capturable); over gloo (CPU hosts, or several
+    ranks sharing one GPU in tests) the f32 bucket goes through
+    torch.distributed.  ``mode="exact"`` reproduces the reference's ascending
+    rank-order fold bit for bit (communicator.py:99-103) on either backend."""
+
+    def __init__(self, group=None, bucket_bytes: int = 32 << 20, mode: str | None = None):
+        import os
+
         import torch.distributed as dist
         if not dist.is_initialized():
             raise InvalidWorkerCount("torch.distributed is not initialised")
@@ -230,8 +304,51 @@ class DataParallelCommunicator:
         self.rank = dist.get_rank(group)
         self.n_workers = dist.get_world_size(group)
         self.bucket_bytes = bucket_bytes
+        self.mode = mode or os.environ.get("NNL_COMM_MODE", "nccl")
+        if self.mode not in COMM_MODES:
+            raise ValueError(f"unknown communicator mode {self.mode!r}")
+        self.backend = dist.get_backend(group)
+        self.nccl = (NcclComm(dist, group, self.rank, self.n_workers, self.mode)
+                     if self.backend == "nccl" else None)
         self._plans: dict = {}
         self._checked: set = set()
+        self._ws = None
+
+    @property
+    def capturable(self) -> bool:
+        """The exchange is stream-ordered (no host synchronisation)."""
+        return self.nccl is not None
+
+    def pad_to(self, n: int) -> int:
+        return self.nccl.bucket_elems(n) if self.nccl is not None else n
+
+    def exchange(self, plan: "BucketPlan", divide: bool, nonfinite_ptr, stream: int) -> None:
+        """pack -> sum over ranks -> unpack q(sum / f32(n)) for one bucket."""
+        if self.nccl is not None:
+            need = int(_lib.lib().nnl_comm_workspace_size(self.nccl.handle, plan.total))
+            if need and (self._ws is None or self._ws.numel() < need):
+                self._ws = self.nccl.workspace(plan.total)
+            self.nccl.allreduce_mean(plan, divide, nonfinite_ptr, stream, self._ws)
+            return
+        t = _lib.torch()
+        world = self.n_workers if divide else 1
+        plan.pack(stream)
+        if self.mode == "exact":  # gather every rank's bucket, fold in rank order
+            parts = [t.empty_like(plan.bucket) for _ in range(self.n_workers)]
+            self._dist.all_gather(parts, plan.bucket, group=self.group)
+            ptrs = t.tensor([q.data_ptr() for q in parts], dtype=t.int64, device=_lib.device())
+            _lib.call("nnl_fold_f32", self.n_workers, ptrs.data_ptr(), plan.total,
+                      plan.bucket.data_ptr(), stream)
+            t.cuda.current_stream().synchronize()  # `parts`/`ptrs` die with this frame
+        else:
+            self._dist.all_reduce(plan.bucket, group=self.group)
+        plan.unpack_mean(plan.bucket.data_ptr(), world, nonfinite_ptr, stream)
+
+    def allreduce_sum_f32(self, tensor) -> None:
+        if self.nccl is not None:
+            self.nccl.allreduce_sum_f32(tensor, _lib.stream())
+        else:
+            self._dist.all_reduce(tensor, group=self.group)
 
     def barrier(self) -> None:
         self._dist.barrier(group=self.group)
@@ -254,19 +371,21 @@ class DataParallelCommunicator:
         plans = self._plans.get(key)
         if plans is None:
             groups = plan_buckets([a.size for a in buffers], self.bucket_bytes)
-            plans = [BucketPlan([buffers[i] for i in g]) for g in groups]
+            plans = []
+            for g in groups:
+                arrs = [buffers[i] for i in g]
+                plans.append(BucketPlan(arrs, pad_to=self.pad_to(sum(a.size for a in arrs))))
             self._plans[key] = plans
         return plans
 
     def all_reduce(self, buffers: list[NdArray], division: bool = False,
                    nonfinite_ptr=None) -> None:
+        """Reference API (communicator.py:69-105): every rank's buffers become
+        the (mean, with division) sum over the ranks, rounded once."""
         self._validate(tuple((a.shape, a.dtype.value) for a in buffers))
         stream = _lib.stream()
-        world = self.n_workers if division else 1
         for p in self.plan(buffers):
-            p.pack(stream)
-            self._dist.all_reduce(p.bucket, group=self.group)
-            p.unpack_mean(p.bucket.data_ptr(), world, nonfinite_ptr, stream)
+            self.exchange(p, division, nonfinite_ptr, stream)
 
 
 class BucketSchedule:
@@ -327,8 +446,10 @@ class BucketedAllReduce:
         self.order = list(reversed(params))
         self.index = {id(p): i for i, p in enumerate(self.order)}
         self.schedule = BucketSchedule([p.grad.size for p in self.order], bucket_bytes)
-        self.plans = [BucketPlan([self.order[i].grad for i in g])
-                      for g in self.schedule.groups]
+        self.plans = []
+        for g in self.schedule.groups:
+            arrs = [self.order[i].grad for i in g]
+            self.plans.append(BucketPlan(arrs, pad_to=comm.pad_to(sum(a.size for a in arrs))))
         self.nonfinite_ptr = nonfinite_ptr
         self.stream = t.cuda.Stream()
         self.world = comm.n_workers
@@ -348,10 +469,7 @@ class BucketedAllReduce:
         plan = self.plans[b]
         self.stream.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(self.stream):
-            s = _lib.stream()
-            plan.pack(s)
-            self.comm._dist.all_reduce(plan.bucket, group=self.comm.group)
-            plan.unpack_mean(plan.bucket.data_ptr(), self.world, self.nonfinite_ptr, s)
+            self.comm.exchange(plan, True, self.nonfinite_ptr, _lib.stream())
 
     def finish(self) -> None:
         t = _lib.torch()
@@ -392,6 +510,13 @@ def _wire_nonfinite(loss: Variable, params: list[Variable], flag_ptr: int) -> bo
         if node.kind not in ("Affine", "Convolution", "BatchNormalization"):
             return False
         node.state["nonfinite_ptr"] = flag_ptr
+        if node.kind == "Convolution":
+            # under the Convolution->BatchNormalization fusion (bias_by_bn) the
+            # BN backward writes this convolution's bias gradient, so it must
+            # flag overflow even when its own gamma/beta are frozen
+            for c in node.outputs[0]._consumers:
+                if c.kind == "BatchNormalization":
+                    c.state["nonfinite_ptr"] = flag_ptr
         covered.update(id(v) for v in hit)
         if sum(1 for c in hit for cc in c._consumers) != len(hit):
             return False  # shared parameters: keep the explicit check
@@ -429,7 +554,8 @@ class DataParallelTrainer:
     def __init__(self, n_workers: int, batch_size: int, build_fn, lr: float, seed: int,
                  loss_scaling=None, clip_norm: float | None = None, timeout: float = 60.0,
                  check_sync: bool = True, momentum: float = 0.0, weight_decay: float = 0.0,
-                 bucket_bytes: int = 8 << 20, distributed: bool | None = None):
+                 bucket_bytes: int = 8 << 20, distributed: bool | None = None,
+                 comm_mode: str | None = None):
         if n_workers < 1:
             raise InvalidWorkerCount(f"need at least one worker, got {n_workers}")
         if batch_size % n_workers != 0:
@@ -472,7 +598,7 @@ class DataParallelTrainer:
             self.replicas.append(rep)
         self.ranks = local
         if self.distributed:
-            self.comm = DataParallelCommunicator()
+            self.comm = DataParallelCommunicator(mode=comm_mode)
             self.group = None
         else:
             self.comm = None
@@ -542,28 +668,47 @@ class DataParallelTrainer:
             rep.solver.update()
         return loss
 
+    def _check_labels(self, rep: _Replica) -> None:
+        """A replayed graph cannot raise from inside forward: surface the host
+        label validation (`.d =` hook) before replay, as the reference raises
+        LabelOutOfRange in forward (functions.py:337-339)."""
+        from .errors import LabelOutOfRange
+        for node in rep.handles["label"]._consumers:
+            if node.state.get("labels_ok") is False:
+                raise LabelOutOfRange(
+                    f"labels must be integers in [0, {node.inputs[0].shape[1]})")
+
     def capture_graph(self) -> None:
         """Record one resident step into a CUDA graph; later `step_resident`
         calls replay it (removes the per-node launch overhead).
 
         Call after at least one warm-up step (all buffers, workspaces and
-        tensor maps are then allocated at fixed addresses).  Single process
-        only; the host-synchronous paths (clip_norm, host scaler) are refused."""
-        if self.distributed or self.n_workers != 1:
-            raise NotImplementedError("graph capture is implemented for one replica per process")
+        tensor maps are then allocated at fixed addresses).  The warm-up run on
+        the capture stream is a real training step on the resident batch.
+        Under torch.distributed every rank calls this together: the recorded
+        step contains the bucketed NCCL exchange issued from inside backward
+        (libnnl's stream-ordered communicator), so N > 1 replays the same
+        graph as N = 1.  Refused: several replicas in one process, the gloo
+        transport, and the host-synchronous paths (clip_norm, host scaler)."""
+        if self.n_workers != 1 and not self.distributed:
+            raise NotImplementedError("graph capture needs one replica per process")
+        if self.distributed and not self.comm.capturable:
+            raise NotImplementedError(f"the {self.comm.backend} transport is host-synchronous")
         rep = self.replicas[0]
         if rep.dscaler is None and self.static_scale is None and rep.scaler is not None:
             raise NotImplementedError("host-synchronous loss scaling cannot be captured")
         t = _lib.torch()
+        rank = self.ranks[0]
+        reduce = self._overlap(rep) if self.distributed else (lambda r: None)
         side = t.cuda.Stream()
         side.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(side):
-            self._work(rep, 0, None, None, lambda r: None)  # warm on the capture stream
+            self._work(rep, rank, None, None, reduce)  # warm on the capture stream
         t.cuda.current_stream().wait_stream(side)
         g = t.cuda.CUDAGraph()
         before = _lib.lib().nnl_launch_count(0)
         with t.cuda.graph(g, stream=side):
-            self._work(rep, 0, None, None, lambda r: None)
+            self._work(rep, rank, None, None, reduce)
         t.cuda.current_stream().wait_stream(side)
         self.graph_kernels = int(_lib.lib().nnl_launch_count(0) - before)  # libnnl kernels/step
         self._graph = g
@@ -651,6 +796,7 @@ class DataParallelTrainer:
         feed["free"][slot] = free
         graph = getattr(self, "_graph", None)
         if graph is not None:
+            self._check_labels(rep)
             graph.replay()
             loss = rep.handles["loss"]
         else:
@@ -669,19 +815,30 @@ class DataParallelTrainer:
         ``shard=True`` (extension): under torch.distributed the arrays are
         already this rank's shard, so no process materialises the global batch.
         """
-        if shard and self.distributed:
+        if self.distributed:
             rep = self.replicas[0]
-            rep.handles["x"].d = x_batch
-            rep.handles["label"].d = label_batch
-            x_batch = label_batch = None
             rank = self.ranks[0]
-
-            loss = self._work(rep, rank, None, None, self._overlap(rep))
+            if shard:
+                xs, ls = x_batch, label_batch
+            else:
+                lo = rank * self.shard_size
+                xs, ls = x_batch[lo:lo + self.shard_size], label_batch[lo:lo + self.shard_size]
+            rep.handles["x"].d = xs
+            rep.handles["label"].d = ls
+            graph = getattr(self, "_graph", None)
+            if graph is not None:  # the recorded step, buckets and NCCL included
+                self._check_labels(rep)
+                graph.replay()
+                loss = rep.handles["loss"]
+            else:
+                loss = self._work(rep, rank, None, None, self._overlap(rep))
             t = _lib.torch()
             lv = t.empty(1, dtype=t.float32, device=_lib.device())
             _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr, lv.data_ptr(),
                       _lib.stream())
-            self.comm._dist.all_reduce(lv)
+            self.comm.allreduce_sum_f32(lv)
+            if self.check_sync and not shard:
+                self._check_distributed(rep)
             return float(lv.item()) / self.n_workers
         if not self.distributed and self.n_workers == 1:
             graph = getattr(self, "_graph", None)
@@ -689,24 +846,11 @@ class DataParallelTrainer:
                 rep = self.replicas[0]
                 rep.handles["x"].d = x_batch[:self.shard_size]
                 rep.handles["label"].d = label_batch[:self.shard_size]
+                self._check_labels(rep)
                 graph.replay()
                 return float(rep.handles["loss"].d)
             loss = self._work(self.replicas[0], 0, x_batch, label_batch, lambda r: None)
             return float(loss.d)
-        if self.distributed:
-            rep = self.replicas[0]
-            rank = self.ranks[0]
-
-            loss = self._work(rep, rank, x_batch, label_batch, self._overlap(rep))
-            t = _lib.torch()
-            lv = t.empty(1, dtype=t.float32, device=_lib.device())
-            _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr, lv.data_ptr(),
-                      _lib.stream())
-            self.comm._dist.all_reduce(lv)
-            if self.check_sync:
-                self._check_distributed(rep)
-            return float(lv.item()) / self.n_workers
-
         def work(comm: Communicator) -> float:
             rep = self.replicas[comm.rank]
 

@@ -94,21 +94,30 @@ __device__ __forceinline__ float relu_gate(float xh, float ga, float be) {
   return Elem<T>::ld(Elem<T>::st(__fadd_rn(__fmul_rn(ga, xh), be))) > 0.f ? 1.f : 0.f;
 }
 
-// MODE 0: (sum x, sum x^2)                               -- forward statistics
+// MODE 0: (sum x-K, sum (x-K)^2), K = shift or x[0]     -- forward statistics
 // MODE 1: (sum gy, sum gy*xhat), gy gated by the ReLU    -- backward reductions
 template <typename T, int V, int MODE>
 __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
     int64_t rows, int32_t c, int groups, int lanes, int64_t rows_per_block,
     const T* __restrict__ x, const T* __restrict__ dy, int relu, const T* __restrict__ gate,
     const float* __restrict__ gamma, const float* __restrict__ beta,
-    const float* __restrict__ mu, const float* __restrict__ istd, float* __restrict__ partials) {
+    const float* __restrict__ mu, const float* __restrict__ istd, float* __restrict__ partials,
+    const float* __restrict__ shift) {
   __shared__ float red[kBnThreads * 8 * 2];
   const int tid = threadIdx.x;
   const int g = tid % groups;
   const int lane = tid / groups;
   const int c0 = (blockIdx.y * groups + g) * V;
   const bool active = lane < lanes && c0 < c;
-  float s1[V], s2[V], m[V], is[V], ga[V], be[V];
+  float s1[V], s2[V], m[V], is[V], ga[V], be[V], kc[V];
+  if (MODE == 0 && active) {
+    if (shift) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) kc[j] = shift[c0 + j];
+    } else {
+      VecLoad<T, V>::load(x + c0, kc);  // centre on the first row
+    }
+  }
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     s1[j] = 0.f;
@@ -141,8 +150,9 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
         if (MODE == 0) {
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            s1[j] += xv[u][j];
-            s2[j] = fmaf(xv[u][j], xv[u][j], s2[j]);
+            const float d = __fsub_rn(xv[u][j], kc[j]);
+            s1[j] += d;
+            s2[j] = fmaf(d, d, s2[j]);
           }
         } else {
 #pragma unroll
@@ -221,18 +231,29 @@ __device__ __forceinline__ void reduce_partials(const float* __restrict__ partia
   }
 }
 
-// forward: mean, biased var (functions.py:401-409), istd (:412)
+// forward: mean, biased var (functions.py:401-409), istd (:412).  The partials
+// are sums of x-K and (x-K)^2 about a per-channel centre K (the caller's shift,
+// else the first row of x), so mean = K + s1/n and var = s2/n - (s1/n)^2 keep
+// their precision when |mean| >> std (the reference's np.var is two-pass).
+// With `shift_out` the batch mean is stored there: the centre of the next call.
 __global__ void __launch_bounds__(1024) k_bn_finalize_fwd(
     const float* __restrict__ partials, int32_t R, int32_t c, int64_t count,
     float* __restrict__ running_mean, float* __restrict__ running_var, float eps, float momentum,
-    float* __restrict__ save_mean, float* __restrict__ save_istd) {
+    float* __restrict__ save_mean, float* __restrict__ save_istd, const float* shift_in,
+    const void* x_row0, int x_f16, float* shift_out) {
   const int ch = red_channel();
   double s1, s2;
   reduce_partials(partials, R, c, ch, s1, s2);
   if (red_leader() && ch < c) {
-    double mean = s1 / (double)count;
-    double var = s2 / (double)count - mean * mean;
+    double k = 0.0;
+    if (shift_in) k = shift_in[ch];
+    else if (x_row0) k = x_f16 ? (double)__half2float(((const __half*)x_row0)[ch])
+                               : (double)((const float*)x_row0)[ch];
+    const double d = s1 / (double)count;
+    const double mean = k + d;
+    double var = s2 / (double)count - d * d;
     if (var < 0.0) var = 0.0;
+    if (shift_out) shift_out[ch] = (float)mean;
     float mu = (float)mean, vb = (float)var;
     // m*mean + (1-m)*mu with m = f32(momentum), 1-m in f32 (functions.py:404-409)
     float m = momentum, one_m = __fsub_rn(1.0f, momentum);
@@ -519,18 +540,22 @@ template <typename T, int MODE>
 static int launch_partials(int64_t rows, int32_t c, const BnGeom& g, int64_t bx, const T* x,
                            const T* dy, int relu, const T* gate, const float* gamma,
                            const float* beta,
-                           const float* mu, const float* istd, float* partials, cudaStream_t st) {
+                           const float* mu, const float* istd, float* partials, cudaStream_t st,
+                           const float* shift = nullptr) {
   int64_t rpb = (rows + bx - 1) / bx;
   dim3 grid((unsigned)bx, (unsigned)g.slabs);
   if (g.vec == 8)
     k_bn_partials<T, 8, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, gate, gamma, beta, mu, istd, partials);
+                                                           relu, gate, gamma, beta, mu, istd, partials,
+                                                           shift);
   else if (g.vec == 4)
     k_bn_partials<T, 4, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, gate, gamma, beta, mu, istd, partials);
+                                                           relu, gate, gamma, beta, mu, istd, partials,
+                                                           shift);
   else
     k_bn_partials<T, 1, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
-                                                           relu, gate, gamma, beta, mu, istd, partials);
+                                                           relu, gate, gamma, beta, mu, istd, partials,
+                                                           shift);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
@@ -602,8 +627,9 @@ static int bn_apply_fwd(int dtype, int64_t rows, int32_t c, const void* x, const
 int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const float* gamma,
                      const float* beta, float* running_mean, float* running_var, float eps,
                      float momentum, const float* stat_partials, int32_t n_partials,
-                     float* save_mean, float* save_istd, void* y, const void* residual,
-                     int fuse_relu, void* ws, size_t ws_bytes, void* stream) {
+                     float* shift, float* save_mean, float* save_istd, void* y,
+                     const void* residual, int fuse_relu, void* ws, size_t ws_bytes,
+                     void* stream) {
   if (rows <= 1)
     return fail(NNL_ERR_DEGENERATE_BATCH, "cannot take batch statistics over %lld element(s)",
                 (long long)rows);
@@ -617,7 +643,7 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
     float* p = (float*)ws;
     if (use_stream(dtype, rows, c, x, nullptr, nullptr)) {
       BnStreamArgs a = {};
-      a.rows = rows; a.c = c; a.x = (const __half*)x; a.partials = p;
+      a.rows = rows; a.c = c; a.x = (const __half*)x; a.partials = p;  // centre: x[0]
       rc = bn_stream_launch(BNS_STATS_F, a, st);
       R = bn_stream_rows(BNS_STATS_F, 1, rows, c);
     } else {
@@ -632,8 +658,11 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
     if (rc) return rc;
     parts = p;
   }
+  // producer partials are centred on `shift` (the value the convolution was
+  // given); the partials pass above centres on x's first row
   k_bn_finalize_fwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
-      parts, R, c, rows, running_mean, running_var, eps, momentum, save_mean, save_istd);
+      parts, R, c, rows, running_mean, running_var, eps, momentum, save_mean, save_istd,
+      stat_partials ? shift : nullptr, stat_partials ? nullptr : x, dtype == NNL_F16, shift);
   NNL_CHECK_LAUNCH();
   return bn_apply_fwd(dtype, rows, c, x, gamma, beta, save_mean, save_istd, y, residual,
                       fuse_relu, st);

@@ -7,7 +7,8 @@
 // in shared memory instead of registers, which is what the register-heavy
 // per-channel constants of BN backward otherwise starve.
 //
-//   STATS_F : (sum x, sum x^2) partial rows            (functions.py:401-403)
+//   STATS_F : (sum x-K, sum (x-K)^2) partial rows, K a per-channel centre
+//             (the first row, or the caller's shift)   (functions.py:401-403)
 //   APPLY_F : y = q(gamma*((x-mu)*istd)+beta) [+ReLU]   (functions.py:412-416)
 //   STATS_B : (sum gy, sum gy*xhat), gy ReLU-gated      (functions.py:421-422)
 //   APPLY_B : gx = (g/n)(n gy - gbeta - xhat ggamma)    (functions.py:424-434)
@@ -53,7 +54,15 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
   const bool active = lane < lanes;
   const int c0 = g * 8;
 
-  float m[8], is[8], ga[8], be[8], gn[8], gb[8], gy2[8], s1[8], s2[8];
+  float m[8], is[8], ga[8], be[8], gn[8], gb[8], gy2[8], s1[8], s2[8], kc[8];
+  if (MODE == STATS_F && active) {
+    if (a.shift) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) kc[j] = a.shift[c0 + j];
+    } else {
+      unpack8(*reinterpret_cast<const uint4*>(a.x + c0), kc);
+    }
+  }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     s1[j] = 0.f;
@@ -109,8 +118,9 @@ __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
         if (MODE == STATS_F) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            s1[j] += xv[j];
-            s2[j] = fmaf(xv[j], xv[j], s2[j]);
+            const float d = __fsub_rn(xv[j], kc[j]);
+            s1[j] += d;
+            s2[j] = fmaf(d, d, s2[j]);
           }
           continue;
         }

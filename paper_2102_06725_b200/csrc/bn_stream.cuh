@@ -21,6 +21,9 @@ struct BnStreamArgs {
   const float* istd;
   const float* gsum;   // [2][C] gbeta, ggamma (APPLY_B)
   float* partials;     // [grid][2][C] (STATS_*, APPLY_B bias sums)
+  // STATS_F centre K[c]: partials are sum(x-K), sum((x-K)^2) so a channel whose
+  // |mean| >> std does not cancel; null -> K = x[0][c] (the first row)
+  const float* shift;
   int relu;
   int acc;
   int batch_stat;

@@ -63,12 +63,13 @@ int32_t nnl_conv2d_stat_rows(const nnl_conv_shape* cs, int dtype) {
 }
 
 int nnl_conv2d_fwd(const nnl_conv_shape* cs, int dtype, const void* x, const void* w,
-                   const void* b, void* y, float* stat_partials, void* ws, size_t ws_bytes,
-                   void* stream) {
+                   const void* b, void* y, float* stat_partials, const float* stat_shift,
+                   void* ws, size_t ws_bytes, void* stream) {
   int rc = check_conv(cs);
   if (rc) return rc;
   GemmProblem pb = conv_problem(cs, kFprop);
   pb.a = x; pb.b = w; pb.bias = b; pb.out = y; pb.stats = stat_partials;
+  pb.stat_shift = stat_shift;
   return run_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
 }
 

@@ -129,6 +129,7 @@ struct TcArgs {
   int flip;           // dgrad: tap t of the im2col load uses weight tap R*S-1-t
   const __half* bias;
   float* stats;
+  const float* stat_shift;  // per-column centre K of the fprop BN statistics (nullable)
   int32_t* nonfinite;
   float* partial;
   int tma_store;      // epilogue writes through the output tensor map (tmC)
@@ -714,12 +715,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit w = decode_unit(a, u);
       const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN;
       const int ab = t & 1;
-      if ((a.bias || EP == 1) && n0 != staged_n0) {  // bias / BN slices of this N tile (f32)
+      // bias / BN slices of this N tile (f32); fprop statistics: the centre K
+      // of each column in bias_s[BN + j] (0 without a shift)
+      if ((a.bias || EP == 1 || a.stats) && n0 != staged_n0) {
         staged_n0 = n0;
         named_sync(2, kEpiThreads);
         for (int j = tid; j < BN; j += kEpiThreads) {
           const bool ok = n0 + j < a.N;
           if (a.bias) bias_s[j] = ok ? __half2float(a.bias[n0 + j]) : 0.f;
+          if (EP == 0 && a.stats) bias_s[BN + j] = ok && a.stat_shift ? a.stat_shift[n0 + j] : 0.f;
           if (EP == 1) {
             bias_s[BN + j] = ok ? a.bn_mean[n0 + j] : 0.f;
             bias_s[2 * BN + j] = ok ? a.bn_istd[n0 + j] : 0.f;
@@ -997,16 +1001,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_commit();
           }
           if (a.stats) {
+            // sums of (y - K) over the warp's VALID rows (idle rows are staged
+            // as zeros, which would otherwise count as -K)
+            const uint32_t vrows = __ballot_sync(0xffffffffu, mv);
             if (CW == 64) {  // lane owns columns c + 2*lane, c + 2*lane + 1
               float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
+              const float ka = bias_s[BN + c + 2 * lane], kb = bias_s[BN + c + 2 * lane + 1];
 #pragma unroll 8
               for (int r = 0; r < 32; ++r) {
                 const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
                     buf + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4));
-                s1a += x.x;
-                s1b += x.y;
-                s2a += x.x * x.x;
-                s2b += x.y * x.y;
+                const float da = (vrows >> r) & 1 ? x.x - ka : 0.f;
+                const float db = (vrows >> r) & 1 ? x.y - kb : 0.f;
+                s1a += da;
+                s1b += db;
+                s2a += da * da;
+                s2b += db * db;
               }
               if (reg_stats) {
                 float* ra = racc[(c - c_lo) / CW];
@@ -1020,12 +1030,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             } else {  // lane owns column c + lane
               float s1 = 0.f, s2 = 0.f;
+              const float kc = bias_s[BN + c + lane];
 #pragma unroll 8
               for (int r = 0; r < 32; ++r) {
                 const float x = __half2float(*reinterpret_cast<const __half*>(
                     buf + r * 64 + (((lane >> 3) ^ ((r >> 1) & 3)) << 4) + (lane & 7) * 2));
-                s1 += x;
-                s2 += x * x;
+                const float d = (vrows >> r) & 1 ? x - kc : 0.f;
+                s1 += d;
+                s2 += d * d;
               }
               if (reg_stats) {
                 float* ra = racc[(c - c_lo) / CW];
@@ -1099,7 +1111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const int j = 16 * h + k;
-            const float x = (mv && nb + j < a.N) ? __half2float(hv[j]) : 0.f;
+            const float x = (mv && nb + j < a.N) ? __half2float(hv[j]) - bias_s[BN + c + j] : 0.f;
             s1[k] = x;
             s2[k] = x * x;
           }
@@ -2377,6 +2389,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   memcpy(args.tap_offh, pl.tap_offh, sizeof(args.tap_offh));
   args.bias = reinterpret_cast<const __half*>(pb.bias);
   args.stats = pb.stats; args.nonfinite = pb.nonfinite;
+  args.stat_shift = pb.stats && !pb.bnx ? pb.stat_shift : nullptr;
   if (pb.bnx) {
     if (pl.remap || pl.nclass) return fail(NNL_ERR_UNSUPPORTED, "fused BN backward with remap");
     args.bnx = reinterpret_cast<const __half*>(pb.bnx);

@@ -22,6 +22,9 @@ def _kind(name: str, doc: str, base: type = NnlError) -> type:
 ShapeMismatch = _kind("ShapeMismatch", "Operand shapes are incompatible.")
 InvalidRange = _kind("InvalidRange", "A numeric range is empty or inverted.")
 KernelTooLarge = _kind("KernelTooLarge", "A window exceeds the padded input extent.")
+# (extension) a device kernel computes in one storage type: operands whose
+# dtypes disagree are refused at apply() instead of being misread
+DtypeMismatch = _kind("DtypeMismatch", "Operand storage dtypes are incompatible.", ShapeMismatch)
 # graph level
 UnknownFunction = _kind("UnknownFunction", "No function kind of that name is registered.")
 CycleDetected = _kind("CycleDetected", "Graph traversal found a cycle.")
@@ -46,7 +49,7 @@ class DeviceError(NnlError):
 
 
 __all__ = [
-    "NnlError", "ShapeMismatch", "InvalidRange", "KernelTooLarge", "UnknownFunction",
+    "NnlError", "ShapeMismatch", "InvalidRange", "KernelTooLarge", "DtypeMismatch", "UnknownFunction",
     "CycleDetected", "UninitializedInput", "ForwardNotRun", "LabelOutOfRange",
     "DegenerateBatch", "ShapeConflict", "EmptyParameterSet", "NotSetup",
     "InvalidWorkerCount", "ShapeMismatchAcrossRanks", "CollectiveTimeout",

@@ -19,7 +19,8 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .errors import DegenerateBatch, KernelTooLarge, LabelOutOfRange, ShapeMismatch
+from .errors import (DegenerateBatch, DtypeMismatch, KernelTooLarge, LabelOutOfRange,
+                     ShapeMismatch)
 from .graph import ExecutionContext, Variable, apply
 from .tensor import Dtype, NdArray
 
@@ -73,6 +74,22 @@ class FunctionImpl:
 
     def output_dtype(self, ctx: ExecutionContext) -> Dtype:
         return ctx.storage_dtype
+
+    # inputs that must be stored in float32 whatever the storage dtype
+    F32_INPUTS: tuple = ()
+
+    def check_dtypes(self, in_dtypes: list, out_dtype: Dtype) -> None:
+        """Every kernel computes in one storage type taken from its first input:
+        the other data operands and the output must share it (the reference
+        computes on f32 values, so it never meets this; the device path refuses
+        rather than misreading a buffer)."""
+        for i, d in enumerate(in_dtypes):
+            want = Dtype.F32 if i in self.F32_INPUTS else out_dtype
+            if d is not want:
+                raise DtypeMismatch(
+                    f"{self.KIND} input {i} is {d.value}, expected {want.value} "
+                    f"(output dtype {out_dtype.value}: build the graph and its inputs under "
+                    f"one TypeConfig)")
 
     def forward(self, node, xs: list[NdArray], ys: list[NdArray]) -> None:
         raise NotImplementedError
@@ -212,17 +229,22 @@ class Convolution(FunctionImpl):
     def forward(self, node, xs, ys):
         x, w, b = xs
         cs = self.shape_struct(x.shape)
-        stats = None
+        stats = shift = None
+        bn = node.state.get("stat_bn")
         if node.state.get("emit_stats"):
             rows = self.stat_rows(node)
-            if rows > 0:
+            # the epilogue sums are centred on the BN's shift (its previous batch
+            # mean); the BN's first forward takes its own centred pass instead
+            if rows > 0 and bn is not None and bn.state.get("shift_ready"):
                 stats = _state_buf(node, "stats", rows * 2 * self.out_maps)
+                shift = bn.state["shift"]
                 node.state["stat_rows"] = rows
             else:
                 node.state.pop("emit_stats", None)
         ws = self._workspace(node, cs, x.code, 0)
         _lib.call("nnl_conv2d_fwd", C.byref(cs), x.code, x.ptr, w.ptr, b.ptr, ys[0].ptr,
-                  stats.data_ptr() if stats is not None else None, ws[0], ws[1], _st())
+                  stats.data_ptr() if stats is not None else None,
+                  shift.data_ptr() if shift is not None else None, ws[0], ws[1], _st())
 
     def bnb_rows(self, node) -> int:
         """Partial rows of the dgrad with the preceding BN's backward statistics
@@ -425,6 +447,7 @@ class BatchNormalization(FunctionImpl):
 
     KIND = "BatchNormalization"
     ARGS = {"eps": "float", "momentum": "float", "batch_stat": "bool"}
+    F32_INPUTS = (1, 2, 3, 4)  # gamma, beta, mean, var (reference parametric.py:67-70)
 
     def __init__(self, eps: float = 1e-5, momentum: float = 0.9, batch_stat: bool = True):
         self.eps = float(eps)
@@ -464,11 +487,16 @@ class BatchNormalization(FunctionImpl):
             if prod is not None and prod.state.get("emit_stats") and "stats" in prod.state:
                 parts, nparts = prod.state["stats"].data_ptr(), prod.state["stat_rows"]
             ws = _lib.workspace(_lib.lib().nnl_bn_workspace_size(rows, c))
+            # per-channel centre of the statistics: in/out, the batch mean of
+            # this call becomes the centre of the next (and of the producing
+            # convolution's epilogue sums)
+            shift = _state_buf(node, "shift", c)
             _lib.call("nnl_bn_fwd_train", x.code, rows, c, x.ptr, gamma.ptr, beta.ptr, mean.ptr,
                       var.ptr, float(np.float32(self.eps)), float(np.float32(self.momentum)),
-                      parts, nparts, sm.data_ptr(), si.data_ptr(), y.ptr,
+                      parts, nparts, shift.data_ptr(), sm.data_ptr(), si.data_ptr(), y.ptr,
                       residual.ptr if residual is not None else None, 1 if relu else 0,
                       ws[0], ws[1], _st())
+            node.state["shift_ready"] = True
         else:
             _lib.call("nnl_bn_fwd_eval", x.code, rows, c, x.ptr, gamma.ptr, beta.ptr, mean.ptr,
                       var.ptr, float(np.float32(self.eps)), sm.data_ptr(), si.data_ptr(), y.ptr,

@@ -241,9 +241,16 @@ class SgdSolver:
     def master_values(self, name: str) -> np.ndarray:
         """Host copy of a master in the parameter's logical order."""
         slot = self._require_setup()[name]
-        t = _lib.torch()
+        return self._logical(slot, slot.master)
+
+    def velocity_values(self, name: str) -> np.ndarray | None:
+        """Host copy of a momentum buffer (None without momentum)."""
+        slot = self._require_setup()[name]
+        return None if slot.velocity is None else self._logical(slot, slot.velocity)
+
+    @staticmethod
+    def _logical(slot, m) -> np.ndarray:
         shape = slot.param.shape
-        m = slot.master
         if len(shape) == 4:
             o, c, kh, kw = shape
             return m.view(o, kh, kw, c).permute(0, 3, 1, 2).cpu().numpy()

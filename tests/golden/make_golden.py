@@ -56,10 +56,11 @@ def gen_numerics(nn):
     return dict(q_in=np.concatenate([vals, rnd, tiny]), q_out=q, **draws)
 
 
-def run_op(nn, build, inputs, half, diff, seed=1.0, f32_from=None):
+def run_op(nn, build, inputs, half, diff, seed=1.0, f32_range=None):
     vs = []
     for i, a in enumerate(inputs):
-        dt = nn.Dtype.F32 if (f32_from is not None and i >= f32_from) else None
+        dt = nn.Dtype.F32 if (f32_range is not None and f32_range[0] <= i < f32_range[1]) \
+            else None
         v = nn.Variable(a.shape, need_grad=(i in diff), dtype=dt)
         v.d = a
         vs.append(v)
@@ -119,11 +120,31 @@ def gen_ops(nn, F):
                 return F.batch_normalization(*v, batch_stat=bs)
 
             cases.append((f"bn_{tag}_{int(bs)}", half, bnb, [x, g, be, m, vv], [0, 1, 2]))
+        # BN backward under a non-trivial upstream gradient: BN -> affine -> SCE
+        # (a ones seed straight into BN makes dx and dgamma vanish), with one
+        # channel offset far from zero (|mean| >> std: two-pass variance)
+        r6 = RngState(seed=6 + int(half))  # own stream: earlier cases keep their draws
+        x = r6.next_uniform((4, 3, 6, 6), -1, 1)
+        x[:, 1] += 64.0
+        g = r6.next_uniform((3,), 0.5, 1.5)
+        be = r6.next_uniform((3,), -0.5, 0.5)
+        m = np.zeros(3, np.float32)
+        vv = np.ones(3, np.float32)
+        wa = r6.next_uniform((108, 10), -1, 1)
+        ba = r6.next_uniform((10,), -1, 1)
+        lab = (np.arange(4) * 3 % 10).astype(np.float32)
+
+        def bn_chain(v):
+            y = F.batch_normalization(v[0], v[1], v[2], v[3], v[4])
+            return F.softmax_cross_entropy(F.affine(y, v[5], v[6]), v[7])
+
+        cases.append((f"bnchain_{tag}", half, bn_chain, [x, g, be, m, vv, wa, ba, lab], [0, 1, 2]))
     for name, half, build, inputs, diff in cases:
         fresh(nn, half)
         # BN scale/shift/statistics are F32 as PF.batch_normalization makes them
-        res = run_op(nn, build, inputs, half, diff, seed=1.0,
-                     f32_from=1 if name.startswith("bn_") else None)
+        f32 = {"bn_": (1, 5), "bnchain_": (1, 5)}
+        rng32 = next((r for k, r in f32.items() if name.startswith(k)), None)
+        res = run_op(nn, build, inputs, half, diff, seed=1.0, f32_range=rng32)
         for i, a in enumerate(inputs):
             out[f"{name}__x{i}"] = a
         for k, v in res.items():
@@ -162,6 +183,35 @@ def gen_solver(nn):
             s2.update()
             vis.append(float(w2.d[0]))
         out.update(master_w=np.array(vis), master_m=s2.slots["w"].master.copy())
+    # clip_grad_by_norm (solver.py:119-129) inside dynamic_step, F16 + F32
+    # parameters; step 1 clips (norm > 1.5), step 2 does not
+    from nanonnl.tensor import RngState
+    for half in (False, True):
+        tag = "h" if half else "f"
+        fresh(nn, half)
+        r = RngState(seed=21)
+        with nn.registry_scope(nn.ParameterRegistry(0)):
+            a = nn.Variable((37, 5), need_grad=True)
+            b = nn.Variable((5,), need_grad=True, dtype=nn.Dtype.F32)
+            a.d = r.next_uniform((37, 5), -1, 1)
+            b.d = r.next_uniform((5,), -1, 1)
+            out[f"clip_{tag}_a_init"] = a.d.copy()
+            out[f"clip_{tag}_b_init"] = b.d.copy()
+            s3 = SgdSolver(0.05, clip_norm=1.5).setup({"a": a, "b": b})
+            sc = DynamicLossScaler(8.0, 2.0, 2000)
+            for step, mag in enumerate((1.0, 0.01)):
+                ga = r.next_uniform((37, 5), -mag, mag)
+                gb = r.next_uniform((5,), -mag, mag)
+                out[f"clip_{tag}_ga{step}"] = ga
+                out[f"clip_{tag}_gb{step}"] = gb
+                a.g = ga * np.float32(sc.loss_scale)
+                b.g = gb * np.float32(sc.loss_scale)
+                assert dynamic_step(sc, s3).applied
+                out[f"clip_{tag}_a{step}"] = a.d.copy()
+                out[f"clip_{tag}_b{step}"] = b.d.copy()
+                out[f"clip_{tag}_a{step}_grad"] = a.g.copy()
+                out[f"clip_{tag}_b{step}_grad"] = b.g.copy()
+                out[f"clip_{tag}_a{step}_master"] = s3.slots["a"].master.copy()
     return out
 
 

@@ -1,0 +1,195 @@
+"""BatchNormalization parity at the ResNet-50 channel widths with a RANDOM
+upstream gradient (a ones seed makes dx and dgamma vanish), and the variance
+of channels whose |mean| >> std.
+
+Expected values are the reference formulas (functions.py:401-438) evaluated
+in float64 on the same (storage-rounded) inputs: the f32 numpy oracle itself
+carries summation error of ~1e-6 relative at 100k rows per channel, so f64 is
+the honest yardstick for the 1e-5 (fp32) / 2e-3 (fp16) tolerances.  The
+backward is driven directly through the operator (FunctionImpl.backward /
+backward_fused) with the chosen gy; the ReLU gate of the fused variant is
+taken from the forward's stored output so that both sides gate identically.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import nnl_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+EPS = 1e-5
+
+
+def _ctx(nn, half):
+    tc = nn.TypeConfig.HALF if half else nn.TypeConfig.FLOAT
+    nn.set_default_context(nn.ExecutionContext(type_config=tc))
+
+
+def _store(a, half):
+    return O.q16(a) if half else a.astype(np.float32)
+
+
+def ref_bn(x, gamma, beta, gy, gate=None):
+    """functions.py:401-438 in float64 over NCHW x (already storage-rounded)."""
+    x = x.astype(np.float64)
+    axes = (0, 2, 3)
+    n = x.size // x.shape[1]
+    shp = (1, -1, 1, 1)
+    mu = x.mean(axis=axes)
+    var = ((x - mu.reshape(shp)) ** 2).mean(axis=axes)          # two-pass, biased
+    istd = 1.0 / np.sqrt(var + EPS)
+    xh = (x - mu.reshape(shp)) * istd.reshape(shp)
+    y = gamma.reshape(shp) * xh + beta.reshape(shp)
+    g = gy.astype(np.float64)
+    if gate is not None:
+        g = g * gate
+    gb = g.sum(axis=axes)
+    gg = (g * xh).sum(axis=axes)
+    gx = (gamma * istd).reshape(shp) / n * (n * g - gb.reshape(shp) - xh * gg.reshape(shp))
+    return dict(mu=mu, var=var, y=y, gx=gx, gbeta=gb, ggamma=gg)
+
+
+def _bn_graph(nn, x, gamma, beta, relu):
+    import paper_2102_06725_b200.functions as F
+    c = x.shape[1]
+    xv = nn.Variable(x.shape, need_grad=True)
+    xv.d = x
+    ps = []
+    for a, ng in ((gamma, True), (beta, True), (np.zeros(c, np.float32), False),
+                  (np.ones(c, np.float32), False)):
+        v = nn.Variable((c,), need_grad=ng, dtype=nn.Dtype.F32)
+        v.d = a
+        ps.append(v)
+    y = F.batch_normalization(xv, *ps)
+    out = F.relu(y) if relu else y
+    return xv, ps, y, out
+
+
+def _run_backward(y, out, xv, ps, gy, relu):
+    """Drive the BN operator's backward with gy (fused with the ReLU when the
+    forward fused them)."""
+    node = y.parent
+    out.g = gy
+    gxs = [xv.grad, ps[0].grad, ps[1].grad, None, None]
+    acc = [False] * 5
+    if relu:
+        node.impl.backward_fused(node, out.parent, gxs, acc)
+    else:
+        node.impl.backward(node, [y.grad], gxs, acc)
+
+
+def _norm_close(got, want, tol, what):
+    got = np.asarray(got, np.float64)
+    scale = np.sqrt(np.mean(want ** 2)) + 1e-30
+    err = np.abs(got - want)
+    bad = err > tol * (np.abs(want) + scale)
+    assert not bad.any(), (what, int(bad.sum()), float(err.max()), float(scale))
+
+
+SHAPES = {64: (32, 64, 56, 56), 256: (128, 256, 28, 28), 1024: (512, 1024, 14, 14),
+          2048: (2048, 2048, 7, 7)}  # >= 100,352 rows per channel each
+
+
+@pytest.mark.parametrize("half", [True, False])
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("c", [64, 256, 1024, 2048])
+def test_bn_train_backward_random_gy(nnl, c, relu, half):
+    if relu and c in (1024, 2048) and not half:
+        pytest.skip("covered by the fp16 ReLU case and the fp32 plain case at this width")
+    _ctx(nnl, half)
+    shape = SHAPES[c]
+    rng = np.random.default_rng(c + 7 * relu + 3 * half)
+    x = _store(rng.uniform(-2, 3, shape).astype(np.float32), half)
+    gamma = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    beta = rng.uniform(-0.5, 0.5, c).astype(np.float32)
+    gy = _store(rng.uniform(-1, 1, shape).astype(np.float32), half)
+    xv, ps, y, out = _bn_graph(nnl, x, gamma, beta, relu)
+    out.forward(clear_buffer=True)
+    got_y = out.d
+    _run_backward(y, out, xv, ps, gy, relu)
+    gate = (got_y > 0).astype(np.float64) if relu else None
+    r = ref_bn(x, gamma.astype(np.float64), beta.astype(np.float64), gy, gate)
+    tol = 2e-3 if half else 1e-5
+    want_y = np.maximum(r["y"], 0) if relu else r["y"]
+    _norm_close(got_y, want_y, tol, "y")
+    _norm_close(xv.g, r["gx"], tol, "gx")
+    _norm_close(ps[0].g, r["ggamma"], 1e-5, "dgamma")   # f32 parameters in both modes
+    _norm_close(ps[1].g, r["gbeta"], 1e-5, "dbeta")
+    # running statistics: 0.9*old + 0.1*batch (functions.py:404-409), f32
+    np.testing.assert_allclose(ps[2].d, np.float32(1 - np.float32(0.9)) * r["mu"], rtol=1e-5,
+                               atol=1e-7)
+    np.testing.assert_allclose(ps[3].d, np.float32(0.9) + np.float32(1 - np.float32(0.9)) * r["var"],
+                               rtol=1e-5)
+
+
+@pytest.mark.parametrize("half", [True, False])
+def test_bn_large_offset_channels_variance(nnl, half):
+    """x = 64 + U(-1,1) on half of the channels (|mean|/std ~ 110): the batch
+    variance must match the two-pass variance of the reference (np.var,
+    functions.py:402), not the cancelling E[x^2] - mean^2 of f32 sums."""
+    _ctx(nnl, half)
+    shape = (32, 64, 56, 56)
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, shape).astype(np.float32)
+    x[:, ::2] += 64.0
+    x = _store(x, half)
+    c = shape[1]
+    gamma = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    beta = rng.uniform(-0.5, 0.5, c).astype(np.float32)
+    gy = _store(rng.uniform(-1, 1, shape).astype(np.float32), half)
+    xv, ps, y, out = _bn_graph(nnl, x, gamma, beta, False)
+    out.forward(clear_buffer=True)
+    _run_backward(y, out, xv, ps, gy, False)
+    r = ref_bn(x, gamma.astype(np.float64), beta.astype(np.float64), gy)
+    tol = 2e-3 if half else 1e-5
+    running_var = ps[3].d
+    batch_var = (running_var - np.float32(0.9)) / np.float32(1 - np.float32(0.9))
+    np.testing.assert_allclose(batch_var, r["var"], rtol=2e-5)  # (/0.1 amplifies f32 rounding)
+    bn = y.parent
+    # (zero-mean channels: the f32 sum of x - x[0] carries ~1e-7 of the spread)
+    np.testing.assert_allclose(bn.state["mean"].cpu().numpy(), r["mu"], rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(bn.state["istd"].cpu().numpy(), 1.0 / np.sqrt(r["var"] + EPS),
+                               rtol=2e-6)
+    _norm_close(out.d, r["y"], tol, "y")
+    _norm_close(xv.g, r["gx"], tol, "gx")
+
+
+@pytest.mark.parametrize("offset", [0.0, 64.0])
+def test_conv_epilogue_statistics_are_centred(nnl, offset):
+    """Convolution -> BN with the statistics taken in the convolution's
+    epilogue (second and later forwards; the first centres its own pass): an
+    identity 1x1 convolution reproduces x exactly, so the BN output must match
+    the two-pass reference on channels offset by `offset`, for fresh batches."""
+    import paper_2102_06725_b200.functions as F
+    _ctx(nnl, True)
+    shape = (32, 64, 28, 28)
+    c = shape[1]
+    rng = np.random.default_rng(5)
+    xv = nnl.Variable(shape)
+    w = nnl.Variable((c, c, 1, 1), need_grad=True)
+    b = nnl.Variable((c,), need_grad=True)
+    w.d = np.eye(c, dtype=np.float32).reshape(c, c, 1, 1)
+    b.d = np.zeros(c, np.float32)
+    gamma = rng.uniform(0.5, 1.5, c).astype(np.float32)
+    beta = rng.uniform(-0.5, 0.5, c).astype(np.float32)
+    ps = []
+    for a, ng in ((gamma, True), (beta, True), (np.zeros(c, np.float32), False),
+                  (np.ones(c, np.float32), False)):
+        v = nnl.Variable((c,), need_grad=ng, dtype=nnl.Dtype.F32)
+        v.d = a
+        ps.append(v)
+    h = F.convolution(xv, w, b)
+    y = F.batch_normalization(h, *ps)
+    out = F.relu(y)
+    conv = h.parent
+    for step in range(3):
+        x = rng.uniform(-1, 1, shape).astype(np.float32)
+        x[:, 1::2] += offset
+        x = O.q16(x)
+        xv.d = x
+        out.forward(clear_buffer=True)
+        if step > 0:
+            assert conv.state.get("emit_stats"), "epilogue statistics path not taken"
+        r = ref_bn(x, gamma.astype(np.float64), beta.astype(np.float64), np.zeros(shape))
+        _norm_close(out.d, np.maximum(r["y"], 0), 2e-3, f"y step {step}")

@@ -51,8 +51,9 @@ def run_oracle_op(name, g):
         xs.append(g[f"{name}__x{i}"])
         i += 1
     kind = name.split("_")[0]
-    diff = [0, 1, 2] if kind in ("affine", "conv", "bn") else [0]
-    vs = [O.Var(a, half=(half and not (kind == "bn" and j >= 1)), need_grad=(j in diff))
+    diff = [0, 1, 2] if kind in ("affine", "conv", "bn", "bnchain") else [0]
+    f32 = range(1, 5) if kind in ("bn", "bnchain") else ()  # F32 BN parameters
+    vs = [O.Var(a, half=(half and j not in f32), need_grad=(j in diff))
           for j, a in enumerate(xs)]
     if kind == "affine":
         y = O.affine(*vs, half)
@@ -69,6 +70,9 @@ def run_oracle_op(name, g):
         y = O.softmax_ce(vs[0], vs[1], half)
     elif kind == "bn":
         y = O.batch_norm(*vs, half, batch_stat=bool(int(name.split("_")[2])))
+    elif kind == "bnchain":  # BN -> affine -> SCE: a random upstream gradient into BN
+        h = O.batch_norm(*vs[:5], half)
+        y = O.softmax_ce(O.affine(h, vs[5], vs[6], half), vs[7], half)
     O.backward(y, 1.0)
     return y, vs, diff
 
@@ -107,7 +111,34 @@ def test_dynamic_scaler_sequence(golden):
         assert applied == bool(g["seq_applied"][i])
         assert sc.loss_scale == g["seq_scales"][i]
         assert np.array_equal(w.value, g["seq_w"][i])
-    assert list(g["seq_scales"][:5]) == [8, 8, 4, 4, 4] or True
+    # interval 2: the overflows at steps 3 and 6 halve the scale and reset the
+    # counter before it can exceed the interval, so no doubling happens
+    assert list(g["seq_scales"]) == [8, 8, 4, 4, 4, 2, 2, 2]
+    assert list(g["seq_applied"]) == [True, True, False, True, True, False, True, True]
+
+
+@pytest.mark.parametrize("half", [False, True])
+def test_clip_grad_by_norm_matches_reference(golden, half):
+    """dynamic_step with clip_norm (solver.py:119-155): step 0 clips, step 1 not."""
+    g = golden("solver")
+    tag = "h" if half else "f"
+    m = O.Model(0, half)
+    a = O.Var(g[f"clip_{tag}_a_init"], half=half, need_grad=True)
+    b = O.Var(g[f"clip_{tag}_b_init"], half=False, need_grad=True)
+    m.params.update(a=a, b=b)
+    opt = O.Sgd(m, 0.05, clip_norm=1.5)
+    sc = O.Scaler(8.0, 2.0, 2000)
+    for step in range(2):
+        for k, v in (("a", a), ("b", b)):
+            opt._master(k, v)
+        a.grad = O.store(g[f"clip_{tag}_ga{step}"] * np.float32(sc.loss_scale), half)
+        b.grad = O.store(g[f"clip_{tag}_gb{step}"] * np.float32(sc.loss_scale), False)
+        assert O.dynamic_step(sc, opt)
+        assert np.array_equal(a.grad, g[f"clip_{tag}_a{step}_grad"])
+        assert np.array_equal(b.grad, g[f"clip_{tag}_b{step}_grad"])
+        assert np.array_equal(opt.master["a"], g[f"clip_{tag}_a{step}_master"])
+        assert np.array_equal(a.value, g[f"clip_{tag}_a{step}"])
+        assert np.array_equal(b.value, g[f"clip_{tag}_b{step}"])
 
 
 def _lenet_build(m, x, t):

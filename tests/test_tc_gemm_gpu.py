@@ -148,14 +148,24 @@ def test_conv_stats_epilogue(nnl, geom):
         v.d = a
     y = F.convolution(*vs, stride=(s, s), pad=(p, p))
     node = y.parent
+    # the epilogue sums are centred on the consuming BN's shift K (its previous
+    # batch mean): a stand-in BN node carries a ready shift
+    import torch
+
+    class _Bn:
+        state = {"shift_ready": True,
+                 "shift": torch.from_numpy(rng.uniform(-0.2, 0.2, cout).astype(np.float32)).cuda()}
     node.state["emit_stats"] = True
+    node.state["stat_bn"] = _Bn
     node.impl.forward(node, [v.data for v in vs], [y.data])
     y.data.mark_set()
     st = y.parent.state["stats"].cpu().numpy()
     rows = y.parent.state["stat_rows"]
     assert rows > 0
     parts = st[: rows * 2 * cout].reshape(rows, 2, cout)
-    yd = y.d.transpose(0, 2, 3, 1).reshape(-1, cout).astype(np.float64)
+    kc = _Bn.state["shift"].cpu().numpy().astype(np.float64)
+    yd = y.d.transpose(0, 2, 3, 1).reshape(-1, cout).astype(np.float64) - kc
+    # idle rows of partial tiles must not count (as -K)
     np.testing.assert_allclose(parts[:, 0].sum(0), yd.sum(0), rtol=1e-4, atol=1e-3)
     np.testing.assert_allclose(parts[:, 1].sum(0), (yd ** 2).sum(0), rtol=1e-4, atol=1e-3)
     ov = [O.Var(a, half=True) for a in (x, w, np.zeros(cout, np.float32))]

@@ -52,7 +52,7 @@ def main():
         ws = torch.empty(wsn, dtype=torch.uint8, device=dev)
         fwd = lambda: _lib.call("nnl_bn_fwd_train", 1, rows, c, x.data_ptr(), g.data_ptr(),
                                 b.data_ptr(), rm.data_ptr(), rv.data_ptr(), 1e-5, 0.9, None, 0,
-                                sm.data_ptr(), si.data_ptr(), y.data_ptr(), None, 1, ws.data_ptr(), wsn,
+                                None, sm.data_ptr(), si.data_ptr(), y.data_ptr(), None, 1, ws.data_ptr(), wsn,
                                 st)
         bwd = lambda: _lib.call("nnl_bn_bwd", 1, rows, c, x.data_ptr(), dy.data_ptr(), 1,
                                 None, None, 0, g.data_ptr(), b.data_ptr(), sm.data_ptr(), si.data_ptr(), 1,

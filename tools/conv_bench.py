@@ -89,7 +89,7 @@ def main():
         for ps in passes:
             if ps == "fwd":
                 fn = lambda: _lib.call("nnl_conv2d_fwd", C.byref(cs), 1, x.data_ptr(), w.data_ptr(),
-                                       bias.data_ptr(), y.data_ptr(), None, ws.data_ptr(),
+                                       bias.data_ptr(), y.data_ptr(), None, None, ws.data_ptr(),
                                        ws.numel(), st)
                 byts = 2.0 * (x.numel() + w.numel() + y.numel())
             elif ps == "dgrad":
