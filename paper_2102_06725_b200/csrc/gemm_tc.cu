@@ -1211,6 +1211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+#ifndef NNL_TC_INSTANTIATE  // helper kernels: host-side TU only
 // out = q(prev + bias + sum_s partial[s][m][n]), fixed split order; `trans`
 // writes D[m][n] to out[n*ldc + m]
 // the same reduction, 4 consecutive columns per thread (plain layout, N and ldc
@@ -1480,6 +1481,8 @@ __global__ void k_zero16(int64_t n8, uint4* __restrict__ p) {
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = make_uint4(0, 0, 0, 0);
 }
+
+#endif  // NNL_TC_INSTANTIATE
 
 // ---------------------------------------------------------------------------
 // host side
@@ -2113,10 +2116,13 @@ static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& t
   return NNL_OK;
 }
 
+// The kernel instantiations of each tile width live in their own translation
+// unit (gemm_tc_bn{64,128,256}.cu include this file with NNL_TC_INSTANTIATE)
+// so that the ~90 variants compile in parallel; this TU holds the host side.
 template <int BN>
-static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
-                       const CUtensorMap& tc, const EpiMaps& em, const TcArgs& args,
-                       cudaStream_t st) {
+int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb,
+                const CUtensorMap& tc, const EpiMaps& em, const TcArgs& args,
+                cudaStream_t st) {
   if (args.bnx) {  // fused BN-backward statistics: dgrad modes, single-CTA tiles <= 128 wide
 #define NNL_TC_BNB(AM, BMD)                                                    \
     if (pl.amode == AM && pl.bmode == BMD && pl.cg == 1 && !pl.resb)           \
@@ -2183,6 +2189,21 @@ static int dispatch_bn(const Plan& pl, const CUtensorMap& ta, const CUtensorMap&
   return fail(NNL_ERR_UNSUPPORTED, "no tcgen05 kernel for mode %d/%d cg %d", pl.amode, pl.bmode,
               pl.cg);
 }
+
+#ifdef NNL_TC_INSTANTIATE
+template int dispatch_bn<NNL_TC_INSTANTIATE>(const Plan&, const CUtensorMap&, const CUtensorMap&,
+                                             const CUtensorMap&, const EpiMaps&, const TcArgs&,
+                                             cudaStream_t);
+#else
+extern template int dispatch_bn<64>(const Plan&, const CUtensorMap&, const CUtensorMap&,
+                                    const CUtensorMap&, const EpiMaps&, const TcArgs&,
+                                    cudaStream_t);
+extern template int dispatch_bn<128>(const Plan&, const CUtensorMap&, const CUtensorMap&,
+                                     const CUtensorMap&, const EpiMaps&, const TcArgs&,
+                                     cudaStream_t);
+extern template int dispatch_bn<256>(const Plan&, const CUtensorMap&, const CUtensorMap&,
+                                     const CUtensorMap&, const EpiMaps&, const TcArgs&,
+                                     cudaStream_t);
 
 bool tc_eligible(const GemmProblem& pb, int dtype) {
   if (dtype != NNL_F16) return false;
@@ -2479,5 +2500,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   }
   return NNL_OK;
 }
+
+#endif  // NNL_TC_INSTANTIATE
 
 }  // namespace nnl
