@@ -56,6 +56,8 @@ int nnl_set_tc_enabled(int enabled);
    2 whenever eligible; returns the previous setting, < 0 only queries
    (initial value from env NNL_TC_PAIRS) */
 int nnl_set_tc_pairs(int enabled);
+/* programmatic dependent launch of every libnnl kernel (default on; NNL_PDL=0) */
+int nnl_set_pdl(int enabled);
 /* weight-stationary tiles (whole B operand resident in shared memory) for
    single-N-tile GEMMs; returns the previous setting, < 0 only queries
    (default on; env NNL_TC_RESB=0) */

@@ -76,6 +76,7 @@ _SIGS = {
     "nnl_launch_count": (i64, [C.c_int]),
     "nnl_set_tc_enabled": (C.c_int, [C.c_int]),
     "nnl_set_tc_pairs": (C.c_int, [C.c_int]),
+    "nnl_set_pdl": (C.c_int, [C.c_int]),
     "nnl_set_tc_resident_b": (C.c_int, [C.c_int]),
     "nnl_set_tc_s2d4": (C.c_int, [C.c_int]),
     "nnl_set_tc_tile4": (C.c_int, [C.c_int]),

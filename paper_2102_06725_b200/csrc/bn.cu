@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_partials(
     const float* __restrict__ gamma, const float* __restrict__ beta,
     const float* __restrict__ mu, const float* __restrict__ istd, float* __restrict__ partials,
     const float* __restrict__ shift) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[kBnThreads * 8 * 2];
   const int tid = threadIdx.x;
   const int g = tid % groups;
@@ -241,6 +243,8 @@ __global__ void __launch_bounds__(1024) k_bn_finalize_fwd(
     float* __restrict__ running_mean, float* __restrict__ running_var, float eps, float momentum,
     float* __restrict__ save_mean, float* __restrict__ save_istd, const float* shift_in,
     const void* x_row0, int x_f16, float* shift_out) {
+  pdl_wait();
+  pdl_trigger();
   const int ch = red_channel();
   double s1, s2;
   reduce_partials(partials, R, c, ch, s1, s2);
@@ -267,6 +271,8 @@ __global__ void __launch_bounds__(1024) k_bn_finalize_fwd(
 __global__ void k_bn_eval_stats(int32_t c, const float* __restrict__ mean,
                                 const float* __restrict__ var, float eps,
                                 float* __restrict__ save_mean, float* __restrict__ save_istd) {
+  pdl_wait();
+  pdl_trigger();
   int ch = blockIdx.x * blockDim.x + threadIdx.x;
   if (ch < c) {
     save_mean[ch] = mean[ch];
@@ -279,6 +285,8 @@ __global__ void __launch_bounds__(1024) k_bn_finalize_bwd(
     const float* __restrict__ partials, int32_t R, int32_t c, float* __restrict__ gsum,
     float* __restrict__ dgamma, int acc_g, float* __restrict__ dbeta, int acc_b,
     int32_t* __restrict__ nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   const int ch = red_channel();
   double s1, s2;
   reduce_partials(partials, R, c, ch, s1, s2);
@@ -345,6 +353,8 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_fwd_apply(
     const T* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     const float* __restrict__ mu, const float* __restrict__ istd, T* __restrict__ y,
     int fuse_relu) {
+  pdl_wait();
+  pdl_trigger();
   const int g = threadIdx.x % groups, lane = threadIdx.x / groups;
   const int c0 = (blockIdx.y * groups + g) * V;
   if (lane >= lanes || c0 >= c) return;
@@ -396,6 +406,8 @@ __global__ void __launch_bounds__(kBnThreads) k_bn_bwd_apply(
     const float* __restrict__ gamma, const float* __restrict__ beta, const float* __restrict__ mu,
     const float* __restrict__ istd, const float* __restrict__ gsum, int batch_stat,
     T* __restrict__ dx, int acc, float* __restrict__ bias_part) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[kBnThreads * 8];
   const int g = threadIdx.x % groups, lane = threadIdx.x / groups;
   const int c0 = (blockIdx.y * groups + g) * V;
@@ -497,6 +509,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024) k_bn_bias_finalize(const float* __restrict__ partials,
                                                            int32_t R, int32_t c, T* __restrict__ db,
                                                            int acc, int32_t* __restrict__ nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   const int ch = red_channel();
   double s1, s2;
   reduce_partials(partials, R, c, ch, s1, s2);
@@ -545,15 +559,15 @@ static int launch_partials(int64_t rows, int32_t c, const BnGeom& g, int64_t bx,
   int64_t rpb = (rows + bx - 1) / bx;
   dim3 grid((unsigned)bx, (unsigned)g.slabs);
   if (g.vec == 8)
-    k_bn_partials<T, 8, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
+    launch_k(k_bn_partials<T, 8, MODE>, grid, kBnThreads, 0, st, rows, c, g.groups, g.lanes, rpb, x, dy,
                                                            relu, gate, gamma, beta, mu, istd, partials,
                                                            shift);
   else if (g.vec == 4)
-    k_bn_partials<T, 4, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
+    launch_k(k_bn_partials<T, 4, MODE>, grid, kBnThreads, 0, st, rows, c, g.groups, g.lanes, rpb, x, dy,
                                                            relu, gate, gamma, beta, mu, istd, partials,
                                                            shift);
   else
-    k_bn_partials<T, 1, MODE><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, dy,
+    launch_k(k_bn_partials<T, 1, MODE>, grid, kBnThreads, 0, st, rows, c, g.groups, g.lanes, rpb, x, dy,
                                                            relu, gate, gamma, beta, mu, istd, partials,
                                                            shift);
   NNL_CHECK_LAUNCH();
@@ -580,10 +594,10 @@ static int launch_fwd_apply(int64_t rows, int32_t c, const BnGeom& g, const T* x
   int64_t rpb = (rows + bx - 1) / bx;
   dim3 grid((unsigned)bx, (unsigned)g.slabs);
   if (g.vec == 8)
-    k_bn_fwd_apply<T, 8><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, gamma,
+    launch_k(k_bn_fwd_apply<T, 8>, grid, kBnThreads, 0, st, rows, c, g.groups, g.lanes, rpb, x, gamma,
                                                       beta, mu, istd, y, fuse_relu);
   else
-    k_bn_fwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(rows, c, g.groups, g.lanes, rpb, x, gamma,
+    launch_k(k_bn_fwd_apply<T, 1>, grid, kBnThreads, 0, st, rows, c, g.groups, g.lanes, rpb, x, gamma,
                                                       beta, mu, istd, y, fuse_relu);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -660,7 +674,7 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
   }
   // producer partials are centred on `shift` (the value the convolution was
   // given); the partials pass above centres on x's first row
-  k_bn_finalize_fwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+  launch_k(k_bn_finalize_fwd, (c + kRedCols - 1) / kRedCols, 1024, 0, st, 
       parts, R, c, rows, running_mean, running_var, eps, momentum, save_mean, save_istd,
       stat_partials ? shift : nullptr, stat_partials ? nullptr : x, dtype == NNL_F16, shift);
   NNL_CHECK_LAUNCH();
@@ -673,7 +687,7 @@ int nnl_bn_fwd_eval(int dtype, int64_t rows, int32_t c, const void* x, const flo
                     float* save_mean, float* save_istd, void* y, const void* residual,
                     int fuse_relu, void* stream) {
   cudaStream_t st = as_stream(stream);
-  k_bn_eval_stats<<<(c + 255) / 256, 256, 0, st>>>(c, mean, var, eps, save_mean, save_istd);
+  launch_k(k_bn_eval_stats, (c + 255) / 256, 256, 0, st, c, mean, var, eps, save_mean, save_istd);
   NNL_CHECK_LAUNCH();
   if (rows * c <= 0) return NNL_OK;
   return bn_apply_fwd(dtype, rows, c, x, gamma, beta, save_mean, save_istd, y, residual,
@@ -719,7 +733,7 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
     });
   }
   if (rc) return rc;
-  k_bn_finalize_bwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+  launch_k(k_bn_finalize_bwd, (c + kRedCols - 1) / kRedCols, 1024, 0, st, 
       parts, (int32_t)bx, c, gsum, dgamma, acc_g, dbeta, acc_b, nonfinite);
   NNL_CHECK_LAUNCH();
   if (dx) {
@@ -744,12 +758,12 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
       dim3 grid((unsigned)bx, (unsigned)g.slabs);
       NNL_DISPATCH_DTYPE(dtype, T, {
         if (g.vec == 4)
-          k_bn_bwd_apply<T, 4><<<grid, kBnThreads, 0, st>>>(
+          launch_k(k_bn_bwd_apply<T, 4>, grid, kBnThreads, 0, st, 
               rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu,
               (const T*)gate, gamma, beta, save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x,
               bp);
         else
-          k_bn_bwd_apply<T, 1><<<grid, kBnThreads, 0, st>>>(
+          launch_k(k_bn_bwd_apply<T, 1>, grid, kBnThreads, 0, st, 
               rows, c, g.groups, g.lanes, rpb, (const T*)x, (const T*)dy, fused_relu,
               (const T*)gate, gamma, beta, save_mean, save_istd, gsum, batch_stat, (T*)dx, acc_x,
               bp);
@@ -758,7 +772,7 @@ int nnl_bn_bwd(int dtype, int64_t rows, int32_t c, const void* x, const void* dy
     }
     if (bp) {
       NNL_DISPATCH_DTYPE(dtype, T, {
-        k_bn_bias_finalize<T><<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+        launch_k(k_bn_bias_finalize<T>, (c + kRedCols - 1) / kRedCols, 1024, 0, st, 
             bp, brows, c, (T*)conv_bias_grad, acc_cb, nonfinite);
       });
       NNL_CHECK_LAUNCH();
@@ -785,7 +799,7 @@ int nnl_bn_bwd_apply(int dtype, int64_t rows, int32_t c, const void* x, const vo
   const int64_t bx = bn_stream_rows(BNS_STATS_B, 2, rows, c);
   float* gsum = (float*)ws + bx * 2 * c;
   float* bparts = gsum + 2 * c;
-  k_bn_finalize_bwd<<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+  launch_k(k_bn_finalize_bwd, (c + kRedCols - 1) / kRedCols, 1024, 0, st, 
       partials, nparts, c, gsum, dgamma, acc_g, dbeta, acc_b, nonfinite);
   NNL_CHECK_LAUNCH();
   if (!dx) return NNL_OK;
@@ -799,7 +813,7 @@ int nnl_bn_bwd_apply(int dtype, int64_t rows, int32_t c, const void* x, const vo
   if (rc) return rc;
   if (bp) {
     const int32_t brows = bn_stream_rows(BNS_APPLY_B, bn_stream_nt(BNS_APPLY_B, a), rows, c);
-    k_bn_bias_finalize<__half><<<(c + kRedCols - 1) / kRedCols, 1024, 0, st>>>(
+    launch_k(k_bn_bias_finalize<__half>, (c + kRedCols - 1) / kRedCols, 1024, 0, st, 
         bp, brows, c, (__half*)conv_bias_grad, acc_cb, nonfinite);
     NNL_CHECK_LAUNCH();
   }

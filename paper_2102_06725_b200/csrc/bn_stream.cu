@@ -42,6 +42,8 @@ __device__ __forceinline__ void unpack8(const uint4& u, float* f) {
 
 template <int MODE, int NT>
 __global__ void __launch_bounds__(kThreads) k_bn_stream(const BnStreamArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kStages = stages(NT);
   constexpr bool kGate = NT == 3;                   // backward, ReLU gate streamed
   constexpr bool kRes = MODE == APPLY_F && NT == 2;  // forward, residual streamed
@@ -262,7 +264,7 @@ int bn_stream_launch(int mode, const BnStreamArgs& in, cudaStream_t st) {
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));   \
       attr[M][NT] = true;                                                                  \
     }                                                                                      \
-    k_bn_stream<M, NT><<<grid, kThreads, smem, st>>>(a);                                   \
+    launch_k(k_bn_stream<M, NT>, grid, kThreads, smem, st, a);                                   \
     NNL_CHECK_LAUNCH();                                                                    \
     return NNL_OK;                                                                         \
   }

@@ -96,6 +96,8 @@ int nccl_ready() {
 // acc[i] = ((in[0][i] + in[1][i]) + in[2][i]) + ...  (ascending rank order, f32)
 __global__ void k_fold_ranks(const float* __restrict__ in, int32_t world, int64_t pitch,
                              int64_t n, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float acc = in[i];
@@ -202,7 +204,7 @@ int nnl_comm_allreduce_mean(nnl_comm* c, const nnl_param_slot* slots, const nnl_
       NNL_NCCL(g_nccl.GroupEnd());
       NNL_CUDA(cudaMemcpyAsync(in + (int64_t)c->rank * slice, bucket + (int64_t)c->rank * slice,
                                slice * sizeof(float), cudaMemcpyDeviceToDevice, st));
-      k_fold_ranks<<<grid_for(slice, 256), 256, 0, st>>>(in, W, slice, slice,
+      launch_k(k_fold_ranks, grid_for(slice, 256), 256, 0, st, in, W, slice, slice,
                                                          bucket + (int64_t)c->rank * slice);
       NNL_CHECK_LAUNCH();
       NNL_NCCL(g_nccl.AllGather(bucket + (int64_t)c->rank * slice, bucket, (size_t)slice,

@@ -18,9 +18,47 @@ void count_launch(int n = 1);
 extern int g_tc_enabled;
 extern int g_tc_pairs;
 
+// ---- programmatic dependent launch (PDL) ---------------------------------
+// Every libnnl kernel is launched with programmatic stream serialization, and
+// every kernel begins with griddepcontrol.wait (the predecessor grid has
+// completed and its writes are visible) followed by launch_dependents: the
+// next kernel's CTAs are scheduled while this one drains, hiding the launch
+// gap between consecutive kernels (also inside CUDA graphs).  NNL_PDL=0 or
+// nnl_set_pdl(0) launches plainly; the waits then return at once.
+extern int g_pdl;
+int pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+extern thread_local cudaError_t t_launch_err;
+
+template <typename... K, typename... A>
+inline void launch_k(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  if (pdl_enabled()) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<K>(args)...);
+  if (e != cudaSuccess) t_launch_err = e;
+}
+
 #define NNL_CHECK_LAUNCH()                                                      \
   do {                                                                          \
     cudaError_t e_ = cudaGetLastError();                                        \
+    if (e_ == cudaSuccess && ::nnl::t_launch_err != cudaSuccess) {              \
+      e_ = ::nnl::t_launch_err;                                                 \
+      ::nnl::t_launch_err = cudaSuccess;                                        \
+    }                                                                           \
     if (e_ != cudaSuccess)                                                      \
       return ::nnl::fail(NNL_ERR_CUDA, "%s:%d %s", __FILE__, __LINE__,          \
                          cudaGetErrorString(e_));                               \

@@ -161,6 +161,12 @@ int nnl_affine_bwd_weight(int dtype, int64_t batch, int64_t in_f, int64_t in_c, 
     pb.g = affine_geom(batch, in_f, in_c, out_f);
     set_extent(pb);
     pb.a = dy; pb.b = x; pb.out = dw; pb.acc = acc_w; pb.out_trans = 1; pb.nonfinite = nonfinite;
+    if (db && !(g_tc_enabled && tc_eligible(pb, dtype))) {
+      // the SIMT kernel takes the bias sums in the same pass (one launch)
+      pb.bias_grad = db;
+      pb.acc_bias = acc_b;
+      return simt_gemm(pb, dtype, ws, ws_bytes, st);
+    }
     rc = run_gemm(pb, dtype, ws, ws_bytes, st);
     if (rc) return rc;
   }

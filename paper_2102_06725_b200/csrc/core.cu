@@ -32,6 +32,16 @@ int fail(int code, const char* fmt, ...) {
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+thread_local cudaError_t t_launch_err = cudaSuccess;
+int g_pdl = -1;
+int pdl_enabled() {
+  if (g_pdl < 0) {
+    const char* e = getenv("NNL_PDL");
+    g_pdl = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_pdl;
+}
+
 // ---------------------------------------------------------------------------
 // vectorised elementwise skeleton: 8 elements (16 B of fp16) per step when the
 // pointers are 16-byte aligned, scalar otherwise.
@@ -41,6 +51,8 @@ __device__ __forceinline__ bool aligned16(const void* p) {
 }
 
 __global__ void k_quantize_f16(int64_t n, const float* __restrict__ x, float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __half2float(__float2half_rn(x[i]));
@@ -48,6 +60,8 @@ __global__ void k_quantize_f16(int64_t n, const float* __restrict__ x, float* __
 
 template <typename T>
 __global__ void k_fill(int64_t n, T* __restrict__ dst, float v) {
+  pdl_wait();
+  pdl_trigger();
   T hv = Elem<T>::st(v);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -56,6 +70,8 @@ __global__ void k_fill(int64_t n, T* __restrict__ dst, float v) {
 
 template <typename T>
 __global__ void k_fill_dev(int64_t n, T* __restrict__ dst, const double* __restrict__ v) {
+  pdl_wait();
+  pdl_trigger();
   // NdArray.fill: np.float32(value) then quantize for F16 (tensor.py:125-131)
   T hv = Elem<T>::st(__double2float_rn(*v));
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -65,6 +81,8 @@ __global__ void k_fill_dev(int64_t n, T* __restrict__ dst, const double* __restr
 
 template <typename T>
 __global__ void k_accumulate(int64_t n, const T* __restrict__ src, T* __restrict__ dst, int acc) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     write_out(dst + i, Elem<T>::load(src + i), acc != 0);
@@ -72,6 +90,8 @@ __global__ void k_accumulate(int64_t n, const T* __restrict__ src, T* __restrict
 
 __global__ void k_accumulate_h8(int64_t n8, const uint4* __restrict__ src, uint4* __restrict__ dst,
                                 int acc) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint4 s = src[i];
@@ -101,6 +121,8 @@ __global__ void k_accumulate_h8(int64_t n8, const uint4* __restrict__ src, uint4
 
 template <typename T>
 __global__ void k_nonfinite(int64_t n, const T* __restrict__ x, int32_t* flag) {
+  pdl_wait();
+  pdl_trigger();
   int bad = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -119,6 +141,8 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 template <typename T>
 __global__ void k_rng_uniform(uint64_t seed, uint64_t counter, int64_t n, double low, double high,
                               T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t base = seed * 0xBF58476D1CE4E5B9ull;
   const double span = __dsub_rn(high, low);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -135,12 +159,16 @@ __device__ __forceinline__ float relu_f(float x) { return (x > 0.f || x != x) ? 
 
 template <typename T>
 __global__ void k_relu_fwd(int64_t n, const T* __restrict__ x, T* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = Elem<T>::st(relu_f(Elem<T>::load(x + i)));
 }
 
 __global__ void k_relu_fwd_h8(int64_t n8, const uint4* __restrict__ x, uint4* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint4 v = x[i];
@@ -154,6 +182,8 @@ __global__ void k_relu_fwd_h8(int64_t n8, const uint4* __restrict__ x, uint4* __
 template <typename T>
 __global__ void k_relu_bwd(int64_t n, const T* __restrict__ x, const T* __restrict__ dy,
                            T* __restrict__ dx, int acc) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float g = __fmul_rn(Elem<T>::load(dy + i), Elem<T>::load(x + i) > 0.f ? 1.f : 0.f);
@@ -163,6 +193,8 @@ __global__ void k_relu_bwd(int64_t n, const T* __restrict__ x, const T* __restri
 
 __global__ void k_relu_bwd_h8(int64_t n8, const uint4* __restrict__ x, const uint4* __restrict__ dy,
                               uint4* __restrict__ dx, int acc) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint4 xv = x[i], gv = dy[i], pv = acc ? dx[i] : make_uint4(0, 0, 0, 0);
@@ -183,6 +215,8 @@ __global__ void k_relu_bwd_h8(int64_t n8, const uint4* __restrict__ x, const uin
 template <typename T>
 __global__ void k_add2(int64_t n, const T* __restrict__ a, const T* __restrict__ b,
                        T* __restrict__ y, int fuse_relu) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float v = Elem<T>::ld(Elem<T>::st(__fadd_rn(Elem<T>::load(a + i), Elem<T>::load(b + i))));
@@ -193,6 +227,8 @@ __global__ void k_add2(int64_t n, const T* __restrict__ a, const T* __restrict__
 
 __global__ void k_add2_h8(int64_t n8, const uint4* __restrict__ a, const uint4* __restrict__ b,
                           uint4* __restrict__ y, int fuse_relu) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint4 av = a[i], bv = b[i], o;
@@ -212,6 +248,8 @@ __global__ void k_add2_h8(int64_t n8, const uint4* __restrict__ a, const uint4* 
 template <typename T>
 __global__ void k_gap_fwd(int64_t n, int64_t hw, int64_t c, const T* __restrict__ x,
                           T* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   int64_t total = n * c;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -226,6 +264,8 @@ __global__ void k_gap_fwd(int64_t n, int64_t hw, int64_t c, const T* __restrict_
 template <typename T>
 __global__ void k_gap_bwd(int64_t n, int64_t hw, int64_t c, const T* __restrict__ dy,
                           T* __restrict__ dx, int acc) {
+  pdl_wait();
+  pdl_trigger();
   int64_t total = n * hw * c;
   const float fhw = (float)hw;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -239,6 +279,8 @@ __global__ void k_gap_bwd(int64_t n, int64_t hw, int64_t c, const T* __restrict_
 // once per channel and writes the hw pixels as 16 B stores
 __global__ void k_gap_bwd_h8(int n, int hw, int c, const __half* __restrict__ dy,
                              __half* __restrict__ dx, int acc) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = c >> 3;
   const float fhw = (float)hw;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * cg; t += gridDim.x * blockDim.x) {
@@ -268,6 +310,8 @@ __global__ void k_gap_bwd_h8(int n, int hw, int c, const __half* __restrict__ dy
 template <typename T>
 __global__ void k_import_narrow(int32_t n, int32_t c, int32_t hw, const float* __restrict__ src,
                                 T* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
   const int total = n * hw;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int b = i / hw, pix = i - b * hw;
@@ -280,6 +324,8 @@ __global__ void k_import_narrow(int32_t n, int32_t c, int32_t hw, const float* _
 template <typename T>
 __global__ void k_import(int32_t n, int32_t c, int32_t hw, const float* __restrict__ src,
                          T* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
   // 32-bit index math (the host guarantees n*c*hw < 2^31)
   const int total = n * c * hw;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -294,6 +340,8 @@ __global__ void k_import(int32_t n, int32_t c, int32_t hw, const float* __restri
 template <typename T>
 __global__ void k_export(int32_t n, int32_t c, int32_t hw, const T* __restrict__ src,
                          float* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
   const int total = n * c * hw;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int pix = i % hw;
@@ -306,6 +354,8 @@ __global__ void k_export(int32_t n, int32_t c, int32_t hw, const T* __restrict__
 
 __global__ void k_fold(int32_t k, const float* const* __restrict__ bufs, int64_t n,
                        float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float acc = bufs[0][i];
@@ -378,6 +428,12 @@ int nnl_set_tc_s2d4(int enabled) {
   if (enabled >= 0) v = enabled ? 1 : 0;
   return prev;
 }
+int nnl_set_pdl(int enabled) {
+  const int prev = pdl_enabled();
+  if (enabled >= 0) g_pdl = enabled ? 1 : 0;
+  return prev;
+}
+
 int nnl_set_tc_pairs(int enabled) {
   if (g_tc_pairs < 0) {
     const char* e = getenv("NNL_TC_PAIRS");
@@ -390,7 +446,7 @@ int nnl_set_tc_pairs(int enabled) {
 
 int nnl_quantize_f16(int64_t n, const float* x, float* y, void* stream) {
   if (n <= 0) return NNL_OK;
-  k_quantize_f16<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, x, y);
+  launch_k(k_quantize_f16, grid_for(n, 256), 256, 0, as_stream(stream), n, x, y);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
@@ -398,7 +454,7 @@ int nnl_quantize_f16(int64_t n, const float* x, float* y, void* stream) {
 int nnl_fill(int dtype, int64_t n, void* dst, float value, void* stream) {
   if (n <= 0) return NNL_OK;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_fill<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, (T*)dst, value);
+    launch_k(k_fill<T>, grid_for(n, 256), 256, 0, as_stream(stream), n, (T*)dst, value);
   });
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -407,7 +463,7 @@ int nnl_fill(int dtype, int64_t n, void* dst, float value, void* stream) {
 int nnl_fill_from_device(int dtype, int64_t n, void* dst, const double* value, void* stream) {
   if (n <= 0) return NNL_OK;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_fill_dev<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, (T*)dst, value);
+    launch_k(k_fill_dev<T>, grid_for(n, 256), 256, 0, as_stream(stream), n, (T*)dst, value);
   });
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -417,11 +473,11 @@ int nnl_accumulate(int dtype, int64_t n, const void* src, void* dst, int accumul
                    void* stream) {
   if (n <= 0) return NNL_OK;
   if (dtype == NNL_F16 && n % 8 == 0 && al16(src) && al16(dst)) {
-    k_accumulate_h8<<<grid_for(n / 8, 256), 256, 0, as_stream(stream)>>>(
+    launch_k(k_accumulate_h8, grid_for(n / 8, 256), 256, 0, as_stream(stream), 
         n / 8, (const uint4*)src, (uint4*)dst, accumulate);
   } else {
     NNL_DISPATCH_DTYPE(dtype, T, {
-      k_accumulate<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, (const T*)src,
+      launch_k(k_accumulate<T>, grid_for(n, 256), 256, 0, as_stream(stream), n, (const T*)src,
                                                                        (T*)dst, accumulate);
     });
   }
@@ -432,7 +488,7 @@ int nnl_accumulate(int dtype, int64_t n, const void* src, void* dst, int accumul
 int nnl_nonfinite(int dtype, int64_t n, const void* x, int32_t* flag, void* stream) {
   if (n <= 0) return NNL_OK;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_nonfinite<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, (const T*)x, flag);
+    launch_k(k_nonfinite<T>, grid_for(n, 256), 256, 0, as_stream(stream), n, (const T*)x, flag);
   });
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -443,7 +499,7 @@ int nnl_rng_uniform(uint64_t seed, uint64_t counter, int64_t n, double low, doub
   if (!(low < high)) return fail(NNL_ERR_INVALID_RANGE, "empty range [%g, %g)", low, high);
   if (n <= 0) return NNL_OK;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_rng_uniform<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(seed, counter, n, low,
+    launch_k(k_rng_uniform<T>, grid_for(n, 256), 256, 0, as_stream(stream), seed, counter, n, low,
                                                                       high, (T*)out);
   });
   NNL_CHECK_LAUNCH();
@@ -453,11 +509,11 @@ int nnl_rng_uniform(uint64_t seed, uint64_t counter, int64_t n, double low, doub
 int nnl_relu_fwd(int dtype, int64_t n, const void* x, void* y, void* stream) {
   if (n <= 0) return NNL_OK;
   if (dtype == NNL_F16 && n % 8 == 0 && al16(x) && al16(y)) {
-    k_relu_fwd_h8<<<grid_for(n / 8, 256), 256, 0, as_stream(stream)>>>(n / 8, (const uint4*)x,
+    launch_k(k_relu_fwd_h8, grid_for(n / 8, 256), 256, 0, as_stream(stream), n / 8, (const uint4*)x,
                                                                        (uint4*)y);
   } else {
     NNL_DISPATCH_DTYPE(dtype, T, {
-      k_relu_fwd<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, (const T*)x, (T*)y);
+      launch_k(k_relu_fwd<T>, grid_for(n, 256), 256, 0, as_stream(stream), n, (const T*)x, (T*)y);
     });
   }
   NNL_CHECK_LAUNCH();
@@ -468,11 +524,11 @@ int nnl_relu_bwd(int dtype, int64_t n, const void* x, const void* dy, void* dx, 
                  void* stream) {
   if (n <= 0) return NNL_OK;
   if (dtype == NNL_F16 && n % 8 == 0 && al16(x) && al16(dy) && al16(dx)) {
-    k_relu_bwd_h8<<<grid_for(n / 8, 256), 256, 0, as_stream(stream)>>>(
+    launch_k(k_relu_bwd_h8, grid_for(n / 8, 256), 256, 0, as_stream(stream), 
         n / 8, (const uint4*)x, (const uint4*)dy, (uint4*)dx, accumulate);
   } else {
     NNL_DISPATCH_DTYPE(dtype, T, {
-      k_relu_bwd<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+      launch_k(k_relu_bwd<T>, grid_for(n, 256), 256, 0, as_stream(stream), 
           n, (const T*)x, (const T*)dy, (T*)dx, accumulate);
     });
   }
@@ -484,11 +540,11 @@ int nnl_add2_fwd(int dtype, int64_t n, const void* a, const void* b, void* y, in
                  void* stream) {
   if (n <= 0) return NNL_OK;
   if (dtype == NNL_F16 && n % 8 == 0 && al16(a) && al16(b) && al16(y)) {
-    k_add2_h8<<<grid_for(n / 8, 256), 256, 0, as_stream(stream)>>>(
+    launch_k(k_add2_h8, grid_for(n / 8, 256), 256, 0, as_stream(stream), 
         n / 8, (const uint4*)a, (const uint4*)b, (uint4*)y, fuse_relu);
   } else {
     NNL_DISPATCH_DTYPE(dtype, T, {
-      k_add2<T><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, (const T*)a, (const T*)b,
+      launch_k(k_add2<T>, grid_for(n, 256), 256, 0, as_stream(stream), n, (const T*)a, (const T*)b,
                                                                  (T*)y, fuse_relu);
     });
   }
@@ -500,7 +556,7 @@ int nnl_gap_fwd(int dtype, int64_t n, int64_t hw, int64_t c, const void* x, void
                 void* stream) {
   if (n * c <= 0) return NNL_OK;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_gap_fwd<T><<<grid_for(n * c, 256), 256, 0, as_stream(stream)>>>(n, hw, c, (const T*)x,
+    launch_k(k_gap_fwd<T>, grid_for(n * c, 256), 256, 0, as_stream(stream), n, hw, c, (const T*)x,
                                                                       (T*)y);
   });
   NNL_CHECK_LAUNCH();
@@ -512,13 +568,13 @@ int nnl_gap_bwd(int dtype, int64_t n, int64_t hw, int64_t c, const void* dy, voi
   if (n * c * hw <= 0) return NNL_OK;
   if (dtype == NNL_F16 && c % 8 == 0 && n * c < (1ll << 31) &&
       !((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx)) & 15)) {
-    k_gap_bwd_h8<<<grid_for(n * (c / 8), 256), 256, 0, as_stream(stream)>>>(
+    launch_k(k_gap_bwd_h8, grid_for(n * (c / 8), 256), 256, 0, as_stream(stream), 
         (int)n, (int)hw, (int)c, (const __half*)dy, (__half*)dx, accumulate);
     NNL_CHECK_LAUNCH();
     return NNL_OK;
   }
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_gap_bwd<T><<<grid_for(n * hw * c, 256), 256, 0, as_stream(stream)>>>(
+    launch_k(k_gap_bwd<T>, grid_for(n * hw * c, 256), 256, 0, as_stream(stream), 
         n, hw, c, (const T*)dy, (T*)dx, accumulate);
   });
   NNL_CHECK_LAUNCH();
@@ -532,10 +588,10 @@ int nnl_import_f32(int dtype, int32_t n, int32_t c, int32_t hw, const float* src
   if (total >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "import of >= 2^31 elements");
   NNL_DISPATCH_DTYPE(dtype, T, {
     if (c <= 4 && hw > 1)
-      k_import_narrow<T><<<grid_for((int64_t)n * hw, 256), 256, 0, as_stream(stream)>>>(
+      launch_k(k_import_narrow<T>, grid_for((int64_t)n * hw, 256), 256, 0, as_stream(stream), 
           n, c, hw, src, (T*)dst);
     else
-      k_import<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(n, c, hw, src, (T*)dst);
+      launch_k(k_import<T>, grid_for(total, 256), 256, 0, as_stream(stream), n, c, hw, src, (T*)dst);
   });
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -547,7 +603,7 @@ int nnl_export_f32(int dtype, int32_t n, int32_t c, int32_t hw, const void* src,
   if (total <= 0) return NNL_OK;
   if (total >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "export of >= 2^31 elements");
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_export<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(n, c, hw, (const T*)src, dst);
+    launch_k(k_export<T>, grid_for(total, 256), 256, 0, as_stream(stream), n, c, hw, (const T*)src, dst);
   });
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -555,7 +611,7 @@ int nnl_export_f32(int dtype, int32_t n, int32_t c, int32_t hw, const void* src,
 
 int nnl_fold_f32(int32_t k, const float* const* bufs_dev, int64_t n, float* out, void* stream) {
   if (n <= 0 || k <= 0) return NNL_OK;
-  k_fold<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(k, bufs_dev, n, out);
+  launch_k(k_fold, grid_for(n, 256), 256, 0, as_stream(stream), k, bufs_dev, n, out);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }

@@ -37,6 +37,8 @@ struct GemmProblem {
   int acc;             // accumulate into out
   int out_trans;       // write D[m][n] at n*M + m (affine wgrad)
   int32_t* nonfinite;  // nullable
+  void* bias_grad = nullptr;  // SIMT affine wgrad: also db[m] (+)= sum_k A(m, k)
+  int acc_bias = 0;
   float* stats;        // fprop BN partials [rows][2][N] about stat_shift, nullable
   const float* stat_shift = nullptr;  // per-column centre K of the fprop statistics
   // dgrad with the following BN's backward statistics fused (TcArgs::bnx ...)

@@ -8,10 +8,20 @@ namespace nnl {
 
 constexpr int kSB = 64, kSK = 16;
 
+// affine problems are plain (permuted-row) matrices: no im2col index math
+__device__ __forceinline__ int64_t affine_row32(const ConvGeom& g, int32_t f) {
+  if (g.ahw == 1) return f;
+  return (int64_t)(f % g.ac) * g.ahw + f / g.ac;
+}
+
 template <typename T>
 __device__ __forceinline__ float fetch_a(const GemmProblem& pb, int64_t m, int64_t k) {
   const ConvGeom& g = pb.g;
   const T* a = (const T*)pb.a;
+  if (g.affine) {
+    // fprop: x[b][f]; dgrad: dy[b][o]; wgrad: dy[b = k][o = m]
+    return pb.mode == kWgrad ? Elem<T>::load(a + k * g.k + m) : Elem<T>::load(a + m * pb.K + k);
+  }
   if (pb.mode == kFprop) {
     int c = (int)(k % g.c);
     int64_t t = k / g.c;
@@ -44,8 +54,12 @@ template <typename T>
 __device__ __forceinline__ float fetch_b(const GemmProblem& pb, int64_t n, int64_t k) {
   const ConvGeom& g = pb.g;
   const T* b = (const T*)pb.b;
+  if (g.affine) {
+    if (pb.mode == kFprop) return Elem<T>::load(b + affine_row32(g, (int32_t)k) * g.k + n);
+    if (pb.mode == kDgrad) return Elem<T>::load(b + affine_row32(g, (int32_t)n) * g.k + k);
+    return Elem<T>::load(b + k * pb.N + n);  // wgrad: x[b = k][f = n]
+  }
   if (pb.mode == kFprop) {
-    if (g.affine) return Elem<T>::load(b + affine_row(g, k) * g.k + n);  // W[i][o]
     return Elem<T>::load(b + n * pb.K + k);
   } else if (pb.mode == kDgrad) {
     if (g.affine) return Elem<T>::load(b + affine_row(g, n) * g.k + k);  // W[i=n][o=k]
@@ -78,6 +92,8 @@ __device__ __forceinline__ void epilogue_store(const GemmProblem& pb, int64_t m,
 template <typename T>
 __global__ void __launch_bounds__(256) k_simt_gemm(GemmProblem pb, int64_t k_per_split,
                                                   float* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float As[kSK][kSB + 4];
   __shared__ float Bs[kSK][kSB + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -110,6 +126,19 @@ __global__ void __launch_bounds__(256) k_simt_gemm(GemmProblem pb, int64_t k_per
     __syncthreads();
   }
   int bad = 0;
+  if (pb.bias_grad && blockIdx.y == 0 && gridDim.z == 1) {
+    // affine bias gradient db[o] = sum_b dy[b][o] (functions.py:116) = the row
+    // sums of A, taken by the first N tile while the operands are hot
+    for (int mm = threadIdx.x; mm < kSB; mm += blockDim.x) {
+      const int64_t m = m0 + mm;
+      if (m >= pb.M) continue;
+      float s = 0.f;
+      for (int64_t k = 0; k < pb.K; ++k) s += fetch_a<T>(pb, m, k);
+      T* db = (T*)pb.bias_grad;
+      write_out(db + m, s, pb.acc_bias != 0);
+      bad |= !isfinite(Elem<T>::load(db + m));
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int64_t m = m0 + ty * 4 + i;
@@ -131,6 +160,8 @@ __global__ void __launch_bounds__(256) k_simt_gemm(GemmProblem pb, int64_t k_per
 // fixed-order split-K reduction + the same epilogue
 template <typename T>
 __global__ void k_splitk_reduce(GemmProblem pb, int splits, const float* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
   int bad = 0;
   const int64_t total = pb.M * pb.N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -143,9 +174,38 @@ __global__ void k_splitk_reduce(GemmProblem pb, int splits, const float* __restr
 }
 
 // bias gradient: per-column f32 partial sums over row chunks, then fixed-order combine
+// narrow outputs (cols <= 128): the block's threads tile (row lanes x cols),
+// so a warp reads whole rows (coalesced) and the lane sums are combined in
+// fixed order in shared memory
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum_partial_narrow(
+    int64_t rows, int cols, int64_t rows_per_block, const T* __restrict__ x,
+    float* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[256];
+  const int lanes = 256 / cols;
+  const int col = threadIdx.x % cols, lane = threadIdx.x / cols;
+  const int64_t r0 = blockIdx.x * rows_per_block;
+  int64_t r1 = r0 + rows_per_block;
+  if (r1 > rows) r1 = rows;
+  float s = 0.f;
+  if (lane < lanes)
+    for (int64_t r = r0 + lane; r < r1; r += lanes) s += Elem<T>::load(x + r * cols + col);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < cols) {
+    float t = 0.f;
+    for (int l = 0; l < lanes; ++l) t += red[l * cols + threadIdx.x];
+    part[blockIdx.x * (int64_t)cols + threadIdx.x] = t;
+  }
+}
+
 template <typename T>
 __global__ void k_colsum_partial(int64_t rows, int64_t cols, int64_t rows_per_block,
                                  const T* __restrict__ x, float* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t col = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
   if (col >= cols) return;
   int64_t r0 = blockIdx.x * rows_per_block, r1 = r0 + rows_per_block;
@@ -158,6 +218,8 @@ __global__ void k_colsum_partial(int64_t rows, int64_t cols, int64_t rows_per_bl
 template <typename T>
 __global__ void k_colsum_final(int64_t cols, int nparts, const float* __restrict__ part,
                                T* __restrict__ out, int acc, int32_t* flag) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int bad = 0;
   if (col < cols) {
@@ -170,9 +232,13 @@ __global__ void k_colsum_final(int64_t cols, int nparts, const float* __restrict
 }
 
 static int simt_splits(const GemmProblem& pb) {
+  if (pb.bias_grad) return 1;  // the fused bias sums need the whole K range
   int64_t tiles = ((pb.M + kSB - 1) / kSB) * ((pb.N + kSB - 1) / kSB);
+  // short reductions run in one pass: a split costs a partial round trip and a
+  // second launch, more than the K loop it shortens
+  if (pb.K <= 2048) return 1;
   int64_t want = (148 * 4 + tiles - 1) / tiles;
-  int64_t max_by_k = (pb.K + 255) / 256;
+  int64_t max_by_k = (pb.K + 511) / 512;
   if (want > max_by_k) want = max_by_k;
   if (want > 64) want = 64;
   if (want < 1) want = 1;
@@ -194,10 +260,10 @@ int simt_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaS
   dim3 grid((unsigned)((pb.M + kSB - 1) / kSB), (unsigned)((pb.N + kSB - 1) / kSB), (unsigned)sp);
   float* partial = sp > 1 ? (float*)ws : nullptr;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_simt_gemm<T><<<grid, 256, 0, st>>>(pb, kps > 0 ? kps : kSK, partial);
+    launch_k(k_simt_gemm<T>, grid, 256, 0, st, pb, kps > 0 ? kps : kSK, partial);
     NNL_CHECK_LAUNCH();
     if (partial) {
-      k_splitk_reduce<T><<<grid_for(pb.M * pb.N, 256), 256, 0, st>>>(pb, sp, partial);
+      launch_k(k_splitk_reduce<T>, grid_for(pb.M * pb.N, 256), 256, 0, st, pb, sp, partial);
       NNL_CHECK_LAUNCH();
     }
   });
@@ -217,9 +283,13 @@ int bias_grad(int dtype, int64_t rows, int64_t cols, const void* dy, void* db, i
   int64_t rpb = (rows + parts - 1) / parts;
   dim3 grid((unsigned)parts, (unsigned)((cols + 127) / 128));
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_colsum_partial<T><<<grid, 128, 0, st>>>(rows, cols, rpb, (const T*)dy, (float*)ws);
+    if (cols <= 128)
+      launch_k(k_colsum_partial_narrow<T>, dim3((unsigned)parts), 256, 0, st, rows, (int)cols,
+               rpb, (const T*)dy, (float*)ws);
+    else
+      launch_k(k_colsum_partial<T>, grid, 128, 0, st, rows, cols, rpb, (const T*)dy, (float*)ws);
     NNL_CHECK_LAUNCH();
-    k_colsum_final<T><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(
+    launch_k(k_colsum_final<T>, (unsigned)((cols + 127) / 128), 128, 0, st, 
         cols, (int)parts, (const float*)ws, (T*)db, acc, nonfinite);
     NNL_CHECK_LAUNCH();
   });

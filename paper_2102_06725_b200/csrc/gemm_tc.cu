@@ -276,6 +276,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (a.tma_store) tma_prefetch(&tmC);
   }
   if (warp == 2) tmem_alloc_cg<CG>(tmem_slot, C::TMEM_COLS);
+  // PDL: the set-up above overlapped the previous kernel's tail; from here on
+  // its outputs are read
+  pdl_wait();
+  pdl_trigger();
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
@@ -1219,6 +1223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void k_tc_splitk_reduce4(int M, int N, int splits, const float* __restrict__ partial,
                                     const __half* __restrict__ bias, __half* __restrict__ out,
                                     int64_t ldc, int acc, int32_t* nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   int bad = 0;
   const int64_t total = (int64_t)M * N, total4 = total / 4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total4;
@@ -1259,6 +1265,8 @@ __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __rest
                                    const __half* __restrict__ bias, __half* __restrict__ out,
                                    int64_t ldc, int acc, int trans, int c4, int c4_s2,
                                    int fr, int fs, int s2d, int32_t* nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   int bad = 0;
   const int64_t total = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -1294,6 +1302,8 @@ __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __rest
 // = x[n][2bp + sr - ph][2bq + sc - pw][ch] (zero outside x and in slots >= 4c)
 __global__ void k_s2d(int nimg, int h, int w, int c, int ph, int pw, int hb, int wb,
                       const __half* __restrict__ x, uint4* __restrict__ xs) {
+  pdl_wait();
+  pdl_trigger();
   const int total = nimg * hb * wb;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int bq = i % wb, t = i / wb;
@@ -1320,6 +1330,8 @@ __global__ void k_s2d(int nimg, int h, int w, int c, int ph, int pw, int hb, int
 // (TMA im2col with 128 B rows instead of four 32 B rows per block row)
 __global__ void k_s2d4(int nimg, int h, int w, int c, int ph, int pw, int hb, int q,
                        const __half* __restrict__ x, uint4* __restrict__ x4) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)nimg * hb * q * 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1349,6 +1361,8 @@ template <int C>
 __global__ void __launch_bounds__(256) k_s2d4_rows(int h, int w, int ph, int pw, int hb, int q,
                                                    const __half* __restrict__ x,
                                                    uint4* __restrict__ x4) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __half srow[];
   const int Y = blockIdx.x % hb, n = blockIdx.x / hb;
   const int rowh = w * C;
@@ -1393,6 +1407,8 @@ __global__ void __launch_bounds__(256) k_s2d4_rows(int h, int w, int ph, int pw,
 // W[k][r][s][c] -> w2[k][(br*s2 + bc)*16 + (sr*2+sc)*c + ch] (the space-to-depth filter)
 __global__ void k_w_s2d(int k, int fr, int fs, int c, int r2, int s2, const __half* __restrict__ w,
                         __half* __restrict__ w2) {
+  pdl_wait();
+  pdl_trigger();
   const int kp = r2 * s2 * 16, total = k * kp;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int col = i % kp, row = i / kp;
@@ -1409,6 +1425,8 @@ __global__ void k_w_s2d(int k, int fr, int fs, int c, int r2, int s2, const __ha
 // zero channel and border padding
 __global__ void k_pad_c4(int pix4, int w, int w4, int off, int c, const __half* __restrict__ x,
                          uint2* __restrict__ x4) {
+  pdl_wait();
+  pdl_trigger();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < pix4; i += gridDim.x * blockDim.x) {
     const int col = i % w4 - off, nh = i / w4;
     __align__(8) __half v[4] = {__float2half(0.f), __float2half(0.f), __float2half(0.f),
@@ -1422,6 +1440,8 @@ __global__ void k_pad_c4(int pix4, int w, int w4, int off, int c, const __half* 
 // W[k][r][s][c] -> wp[k][kp] with wp[k][(r*s2 + s)*4 + c], zeros elsewhere
 __global__ void k_pad_w_c4(int k, int fr, int fs, int s2, int c, int kp,
                            const __half* __restrict__ w, __half* __restrict__ wp) {
+  pdl_wait();
+  pdl_trigger();
   const int total = k * kp;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int col = i % kp, row = i / kp;
@@ -1436,6 +1456,8 @@ __global__ void k_pad_w_c4(int k, int fr, int fs, int s2, int c, int kp,
 // kp.  One thread per (row m, 8-wide k chunk), 32-bit index math, 16 B stores.
 __global__ void k_im2col(ConvGeom g, int M, int kp, const __half* __restrict__ x,
                          __half* __restrict__ col) {
+  pdl_wait();
+  pdl_trigger();
   const int rsc = g.r * g.s * g.c;
   const int kc = kp >> 3;
   const int total = M * kc;
@@ -1469,6 +1491,8 @@ __global__ void k_im2col(ConvGeom g, int M, int kp, const __half* __restrict__ x
 
 __global__ void k_pad_rows(int rows, int cols, int kp, const __half* __restrict__ src,
                            __half* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
   const int total = rows * kp;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int k = i % kp, r = i / kp;
@@ -1477,6 +1501,8 @@ __global__ void k_pad_rows(int rows, int cols, int kp, const __half* __restrict_
 }
 
 __global__ void k_zero16(int64_t n8, uint4* __restrict__ p) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = make_uint4(0, 0, 0, 0);
@@ -2102,15 +2128,22 @@ static int launch_tc(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& t
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int na = 0;
   if (CG == 2) {
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (pdl_enabled()) {  // (common.cuh: programmatic dependent launch)
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   NNL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, em, args));
   count_launch();
   return NNL_OK;
@@ -2283,7 +2316,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const __half* src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
     const int64_t rows = (int64_t)g.n * g.p * g.q;
     if (rows * (pl.kp / 8) >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "im2col too large");
-    k_im2col<<<grid_for(rows * (pl.kp / 8), 256, 148 * 16), 256, 0, st>>>(g, (int)rows, pl.kp,
+    launch_k(k_im2col, grid_for(rows * (pl.kp / 8), 256, 148 * 16), 256, 0, st, g, (int)rows, pl.kp,
                                                                           src, col);
     NNL_CHECK_LAUNCH();
     if (pb.mode == kFprop) pl.A.ptr = col; else pl.B.ptr = col;
@@ -2313,21 +2346,21 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const bool rows = pl.s2d4 && g.w * g.c * 4 <= 48 * 1024;
 #define NNL_S2D4_ROWS(CC)                                                                  \
     if (rows && g.c == CC)                                                                 \
-      k_s2d4_rows<CC><<<g.n * pl.g2.h, 256, g.w * g.c * 4, st>>>(                          \
+      launch_k(k_s2d4_rows<CC>, g.n * pl.g2.h, 256, g.w * g.c * 4, st,                           \
           g.h, g.w, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
     NNL_S2D4_ROWS(1) else NNL_S2D4_ROWS(2) else NNL_S2D4_ROWS(3) else NNL_S2D4_ROWS(4)
     else if (pl.s2d4)
-      k_s2d4<<<grid_for(pix * 4, 256, 148 * 16), 256, 0, st>>>(
+      launch_k(k_s2d4, grid_for(pix * 4, 256, 148 * 16), 256, 0, st, 
           g.n, g.h, g.w, g.c, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
     else
-      k_s2d<<<grid_for(pix, 256, 148 * 16), 256, 0, st>>>(
+      launch_k(k_s2d, grid_for(pix, 256, 148 * 16), 256, 0, st, 
           g.n, g.h, g.w, g.c, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
     NNL_CHECK_LAUNCH();
     pl.im.ptr = xs;
     pl.sp_a = xs;
     if (pb.mode == kFprop) {
       const int total = g.k * pl.kp;
-      k_w_s2d<<<grid_for(total, 256), 256, 0, st>>>(g.k, g.r, g.s, g.c, pl.g2.r, pl.s2,
+      launch_k(k_w_s2d, grid_for(total, 256), 256, 0, st, g.k, g.r, g.s, g.c, pl.g2.r, pl.s2,
                                                      reinterpret_cast<const __half*>(pb.b), wpad);
       NNL_CHECK_LAUNCH();
       pl.B.ptr = wpad;
@@ -2337,13 +2370,13 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const __half* src = reinterpret_cast<const __half*>(pb.mode == kFprop ? pb.a : pb.b);
     const int64_t pix = (int64_t)g.n * g.h * pl.c4_w4;
     if (pix >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "narrow-channel input too large");
-    k_pad_c4<<<grid_for(pix, 256, 148 * 16), 256, 0, st>>>(
+    launch_k(k_pad_c4, grid_for(pix, 256, 148 * 16), 256, 0, st, 
         (int)pix, g.w, pl.c4_w4, pl.c4_off, g.c, src, reinterpret_cast<uint2*>(x4));
     NNL_CHECK_LAUNCH();
     pl.gsrc = x4;
     if (pb.mode == kFprop) {
       const int total = g.k * pl.kp;
-      k_pad_w_c4<<<grid_for(total, 256), 256, 0, st>>>(g.k, g.r, g.s, pl.c4_s2, g.c, pl.kp,
+      launch_k(k_pad_w_c4, grid_for(total, 256), 256, 0, st, g.k, g.r, g.s, pl.c4_s2, g.c, pl.kp,
                                                         reinterpret_cast<const __half*>(pb.b), wpad);
       NNL_CHECK_LAUNCH();
       pl.B.ptr = wpad;
@@ -2351,7 +2384,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   }
   if (pl.pad_w) {
     const int total = g.k * pl.kp;
-    k_pad_rows<<<grid_for(total, 256), 256, 0, st>>>(g.k, (int)(g.r * g.s * g.c), pl.kp,
+    launch_k(k_pad_rows, grid_for(total, 256), 256, 0, st, g.k, (int)(g.r * g.s * g.c), pl.kp,
                                                       reinterpret_cast<const __half*>(pb.b), wpad);
     NNL_CHECK_LAUNCH();
     pl.B.ptr = wpad;
@@ -2360,7 +2393,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const int64_t n8 = (int64_t)g.n * g.h * g.w * g.c / 8;
     if ((g.c % 8) || (reinterpret_cast<uintptr_t>(pb.out) & 15))
       return fail(NNL_ERR_UNSUPPORTED, "strided dgrad output not 16 B aligned");
-    k_zero16<<<grid_for(n8, 256), 256, 0, st>>>(n8, reinterpret_cast<uint4*>(pb.out));
+    launch_k(k_zero16, grid_for(n8, 256), 256, 0, st, n8, reinterpret_cast<uint4*>(pb.out));
     NNL_CHECK_LAUNCH();
   }
   CUtensorMap ta, tb;
@@ -2487,11 +2520,11 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const int c4 = mapped ? g.c : 0;
     if (!mapped && pl.N % 4 == 0 && pl.ldc % 4 == 0 &&
         !(reinterpret_cast<uintptr_t>(pb.out) & 7))
-      k_tc_splitk_reduce4<<<grid_for((int64_t)pl.M * pl.N / 4, 256), 256, 0, st>>>(
+      launch_k(k_tc_splitk_reduce4, grid_for((int64_t)pl.M * pl.N / 4, 256), 256, 0, st, 
           pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
           reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, pb.nonfinite);
     else
-      k_tc_splitk_reduce<<<grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st>>>(
+      launch_k(k_tc_splitk_reduce, grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st, 
           pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
           reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, 0, c4,
           pl.s2d ? pl.s2 : pl.c4_s2, g.r, g.s, pl.s2d && pb.mode == kWgrad ? 1 : 0,

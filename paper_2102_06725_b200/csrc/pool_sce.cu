@@ -13,6 +13,8 @@ namespace nnl {
 template <typename T>
 __global__ void k_maxpool_fwd(nnl_pool_shape ps, const T* __restrict__ x, T* __restrict__ y,
                               uint8_t* __restrict__ arg) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)ps.n * ps.p * ps.q * ps.c;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -55,6 +57,8 @@ __global__ void k_maxpool_fwd(nnl_pool_shape ps, const T* __restrict__ x, T* __r
 template <typename T>
 __global__ void k_maxpool_bwd(nnl_pool_shape ps, const T* __restrict__ dy,
                               const uint8_t* __restrict__ arg, T* __restrict__ dx, int acc) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)ps.n * ps.h * ps.w * ps.c;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -93,6 +97,8 @@ __global__ void k_maxpool_bwd(nnl_pool_shape ps, const T* __restrict__ dy,
 // semantics as the scalar kernels above.
 __global__ void k_maxpool_fwd_h8(nnl_pool_shape ps, const uint4* __restrict__ x,
                                  uint4* __restrict__ y, uint2* __restrict__ arg) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = ps.c >> 3;
   const int total = ps.n * ps.p * ps.q * cg;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -212,6 +218,8 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd_k3s2(nnl_pool_shape ps,
                                                           const uint4* __restrict__ x,
                                                           uint4* __restrict__ y,
                                                           uint2* __restrict__ arg) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = ps.c >> 3;
   const int total = ps.n * ps.p * ps.q * cg;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -248,6 +256,8 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd_k3s2_rows(nnl_pool_shape ps
                                                                const uint4* __restrict__ x,
                                                                uint4* __restrict__ y,
                                                                uint2* __restrict__ arg) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint4 rows[];
   const int cg = ps.c >> 3, rowv = ps.w * cg;
   const int op = blockIdx.x % ps.p, b = blockIdx.x / ps.p;
@@ -298,6 +308,8 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_k3s2p1(nnl_pool_shape ps,
                                                             const uint4* __restrict__ dy,
                                                             const uint2* __restrict__ arg,
                                                             uint4* __restrict__ dx, int acc) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = ps.c >> 3;
   const int hb = (ps.h + 1) >> 1, wb = (ps.w + 1) >> 1;
   const int total = ps.n * hb * wb * cg;
@@ -359,6 +371,8 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_k3s2p1(nnl_pool_shape ps,
 
 __global__ void k_maxpool_bwd_h8(nnl_pool_shape ps, const uint4* __restrict__ dy,
                                  const uint2* __restrict__ arg, uint4* __restrict__ dx, int acc) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = ps.c >> 3;
   const int total = ps.n * ps.h * ps.w * cg;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -409,6 +423,8 @@ template <typename T>
 __global__ void k_sce_rows(int64_t batch, int64_t classes, const T* __restrict__ logits,
                            const T* __restrict__ labels, float* __restrict__ row_stats,
                            int32_t* __restrict__ label_err) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= batch) return;
@@ -439,6 +455,8 @@ __global__ void k_sce_rows(int64_t batch, int64_t classes, const T* __restrict__
 // loss = q(-(sum_b logp[b, t_b]) / B)  (functions.py:346; one block, fixed order)
 template <typename T>
 __global__ void k_sce_loss(int64_t batch, const float* __restrict__ row_stats, T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float part[32];
   float s = 0.f;
   for (int64_t i = threadIdx.x; i < batch; i += blockDim.x) s += row_stats[3 * i + 2];
@@ -458,6 +476,8 @@ template <typename T>
 __global__ void k_sce_bwd(int64_t batch, int64_t classes, const T* __restrict__ logits,
                           const T* __restrict__ labels, const float* __restrict__ row_stats,
                           const T* __restrict__ gloss, T* __restrict__ g, int acc) {
+  pdl_wait();
+  pdl_trigger();
   const float scale = __fdiv_rn(Elem<T>::load(gloss), (float)batch);
   const int64_t total = batch * classes;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -490,19 +510,19 @@ int nnl_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x, void* y,
     static const bool staged = getenv("NNL_POOL_ROWS") && getenv("NNL_POOL_ROWS")[0] == '1';
     if (staged && ps->kh == 3 && ps->kw == 3 && ps->sh == 2 && ps->sw == 2 &&
         rows_bytes <= 48 * 1024)
-      k_maxpool_fwd_k3s2_rows<<<ps->n * ps->p, 256, rows_bytes, as_stream(stream)>>>(
+      launch_k(k_maxpool_fwd_k3s2_rows, ps->n * ps->p, 256, rows_bytes, as_stream(stream), 
           *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
     else if (ps->kh == 3 && ps->kw == 3 && ps->sh == 2 && ps->sw == 2)
-      k_maxpool_fwd_k3s2<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+      launch_k(k_maxpool_fwd_k3s2, grid_for(total / 8, 256), 256, 0, as_stream(stream), 
           *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
     else
-      k_maxpool_fwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+      launch_k(k_maxpool_fwd_h8, grid_for(total / 8, 256), 256, 0, as_stream(stream), 
           *ps, (const uint4*)x, (uint4*)y, (uint2*)argmax);
     NNL_CHECK_LAUNCH();
     return NNL_OK;
   }
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_maxpool_fwd<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(*ps, (const T*)x,
+    launch_k(k_maxpool_fwd<T>, grid_for(total, 256), 256, 0, as_stream(stream), *ps, (const T*)x,
                                                                           (T*)y, argmax);
   });
   NNL_CHECK_LAUNCH();
@@ -518,19 +538,18 @@ int nnl_maxpool_bwd(int dtype, const nnl_pool_shape* ps, const void* dy, const u
       ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) |
         reinterpret_cast<uintptr_t>(argmax)) & 15) == 0) {
     if (ps->kh == 3 && ps->kw == 3 && ps->sh == 2 && ps->sw == 2 && ps->ph == 1 && ps->pw == 1)
-      k_maxpool_bwd_k3s2p1<<<grid_for((int64_t)ps->n * ((ps->h + 1) / 2) * ((ps->w + 1) / 2) *
-                                          (ps->c / 8), 256),
-                             256, 0, as_stream(stream)>>>(*ps, (const uint4*)dy,
+      launch_k(k_maxpool_bwd_k3s2p1, grid_for((int64_t)ps->n * ((ps->h + 1) / 2) * ((ps->w + 1) / 2) *
+                                          (ps->c / 8), 256), 256, 0, as_stream(stream), *ps, (const uint4*)dy,
                                                           (const uint2*)argmax, (uint4*)dx,
                                                           accumulate);
     else
-      k_maxpool_bwd_h8<<<grid_for(total / 8, 256), 256, 0, as_stream(stream)>>>(
+      launch_k(k_maxpool_bwd_h8, grid_for(total / 8, 256), 256, 0, as_stream(stream), 
           *ps, (const uint4*)dy, (const uint2*)argmax, (uint4*)dx, accumulate);
     NNL_CHECK_LAUNCH();
     return NNL_OK;
   }
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_maxpool_bwd<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+    launch_k(k_maxpool_bwd<T>, grid_for(total, 256), 256, 0, as_stream(stream), 
         *ps, (const T*)dy, argmax, (T*)dx, accumulate);
   });
   NNL_CHECK_LAUNCH();
@@ -542,10 +561,10 @@ int nnl_sce_fwd(int dtype, int64_t batch, int64_t classes, const void* logits, c
   if (batch <= 0 || classes <= 0) return fail(NNL_ERR_SHAPE_MISMATCH, "empty logits");
   NNL_DISPATCH_DTYPE(dtype, T, {
     int warps = 8;
-    k_sce_rows<T><<<(int)((batch + warps - 1) / warps), warps * 32, 0, as_stream(stream)>>>(
+    launch_k(k_sce_rows<T>, (int)((batch + warps - 1) / warps), warps * 32, 0, as_stream(stream), 
         batch, classes, (const T*)logits, (const T*)labels, row_stats, label_err);
     NNL_CHECK_LAUNCH();
-    k_sce_loss<T><<<1, 256, 0, as_stream(stream)>>>(batch, row_stats, (T*)loss_out);
+    launch_k(k_sce_loss<T>, 1, 256, 0, as_stream(stream), batch, row_stats, (T*)loss_out);
   });
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -557,7 +576,7 @@ int nnl_sce_bwd(int dtype, int64_t batch, int64_t classes, const void* logits, c
   int64_t total = batch * classes;
   if (total <= 0) return NNL_OK;
   NNL_DISPATCH_DTYPE(dtype, T, {
-    k_sce_bwd<T><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+    launch_k(k_sce_bwd<T>, grid_for(total, 256), 256, 0, as_stream(stream), 
         batch, classes, (const T*)logits, (const T*)labels, row_stats, (const T*)gloss,
         (T*)glogits, accumulate);
   });

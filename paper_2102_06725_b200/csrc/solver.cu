@@ -34,6 +34,8 @@ __device__ __forceinline__ void store_any(void* p, int dtype, int64_t i, float v
 __global__ void k_multi_nonfinite(const nnl_param_slot* __restrict__ slots,
                                   const nnl_chunk* __restrict__ chunks, int32_t n_chunks,
                                   int32_t* flag) {
+  pdl_wait();
+  pdl_trigger();
   int bad = 0;
   for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
     bad |= !isfinite(load_any(slots[s].grad, slots[s].dtype, i));
@@ -44,6 +46,8 @@ __global__ void k_multi_nonfinite(const nnl_param_slot* __restrict__ slots,
 __global__ void k_multi_scale(const nnl_param_slot* __restrict__ slots,
                               const nnl_chunk* __restrict__ chunks, int32_t n_chunks,
                               float factor) {
+  pdl_wait();
+  pdl_trigger();
   for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
     const nnl_param_slot& p = slots[s];
     store_any(p.grad, p.dtype, i, __fmul_rn(load_any(p.grad, p.dtype, i), factor));
@@ -53,6 +57,8 @@ __global__ void k_multi_scale(const nnl_param_slot* __restrict__ slots,
 __global__ void k_multi_sumsq(const nnl_param_slot* __restrict__ slots,
                               const nnl_chunk* __restrict__ chunks, int32_t n_chunks,
                               double* out) {
+  pdl_wait();
+  pdl_trigger();
   double acc = 0.0;
   for_chunks(chunks, n_chunks, [&](int32_t, int32_t s, int64_t i) {
     float g = load_any(slots[s].grad, slots[s].dtype, i);
@@ -95,6 +101,8 @@ __device__ __forceinline__ float update_elem(float g, bool f16, bool scaled, flo
 __global__ void k_multi_update(const nnl_param_slot* __restrict__ slots,
                                const nnl_chunk* __restrict__ chunks, int32_t n_chunks, float lr,
                                float momentum, float wd, const nnl_scaler_state* scaler) {
+  pdl_wait();
+  pdl_trigger();
   float factor = 1.0f;
   if (scaler) {
     if (scaler->nonfinite) return;  // SkippedInfNan: bytes stay unchanged
@@ -169,6 +177,8 @@ __global__ void k_multi_update(const nnl_param_slot* __restrict__ slots,
 }
 
 __global__ void k_scaler_finish(nnl_scaler_state* s) {
+  pdl_wait();
+  pdl_trigger();
   if (s->nonfinite) {
     s->loss_scale = s->loss_scale / s->scaling_factor;
     s->counter = 0;
@@ -190,6 +200,8 @@ __global__ void k_bucket_pack(const nnl_param_slot* __restrict__ slots,
                               const nnl_chunk* __restrict__ chunks,
                               const int64_t* __restrict__ pos, int32_t n_chunks,
                               float* __restrict__ bucket) {
+  pdl_wait();
+  pdl_trigger();
   for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
     const nnl_chunk ch = chunks[ci];
     const nnl_param_slot& p = slots[ch.slot];
@@ -223,6 +235,8 @@ __global__ void k_bucket_unpack(const nnl_param_slot* __restrict__ slots,
                                 const nnl_chunk* __restrict__ chunks,
                                 const int64_t* __restrict__ pos, int32_t n_chunks,
                                 const float* __restrict__ bucket, float world, int32_t* flag) {
+  pdl_wait();
+  pdl_trigger();
   int bad = 0;
   for (int32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
     const nnl_chunk ch = chunks[ci];
@@ -270,7 +284,7 @@ extern "C" {
 int nnl_multi_nonfinite(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
                         int32_t* flag, void* stream) {
   if (n_chunks <= 0) return NNL_OK;
-  k_multi_nonfinite<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, n_chunks,
+  launch_k(k_multi_nonfinite, chunk_grid(n_chunks), 256, 0, as_stream(stream), slots, chunks, n_chunks,
                                                                         flag);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -279,7 +293,7 @@ int nnl_multi_nonfinite(const nnl_param_slot* slots, const nnl_chunk* chunks, in
 int nnl_multi_scale_grad(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
                          float factor, void* stream) {
   if (n_chunks <= 0) return NNL_OK;
-  k_multi_scale<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, n_chunks,
+  launch_k(k_multi_scale, chunk_grid(n_chunks), 256, 0, as_stream(stream), slots, chunks, n_chunks,
                                                                     factor);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -288,7 +302,7 @@ int nnl_multi_scale_grad(const nnl_param_slot* slots, const nnl_chunk* chunks, i
 int nnl_multi_sumsq(const nnl_param_slot* slots, const nnl_chunk* chunks, int32_t n_chunks,
                     double* out, void* stream) {
   if (n_chunks <= 0) return NNL_OK;
-  k_multi_sumsq<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, n_chunks,
+  launch_k(k_multi_sumsq, chunk_grid(n_chunks), 256, 0, as_stream(stream), slots, chunks, n_chunks,
                                                                     out);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -298,14 +312,14 @@ int nnl_multi_sgd_update(const nnl_param_slot* slots, const nnl_chunk* chunks, i
                          float lr, float momentum, float weight_decay, nnl_scaler_state* scaler,
                          void* stream) {
   if (n_chunks <= 0) return NNL_OK;
-  k_multi_update<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(
+  launch_k(k_multi_update, chunk_grid(n_chunks), 256, 0, as_stream(stream), 
       slots, chunks, n_chunks, lr, momentum, weight_decay, scaler);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
 
 int nnl_scaler_finish(nnl_scaler_state* scaler, void* stream) {
-  k_scaler_finish<<<1, 1, 0, as_stream(stream)>>>(scaler);
+  launch_k(k_scaler_finish, 1, 1, 0, as_stream(stream), scaler);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
@@ -313,7 +327,7 @@ int nnl_scaler_finish(nnl_scaler_state* scaler, void* stream) {
 int nnl_bucket_pack(const nnl_param_slot* slots, const nnl_chunk* chunks, const int64_t* chunk_pos,
                     int32_t n_chunks, float* bucket, void* stream) {
   if (n_chunks <= 0) return NNL_OK;
-  k_bucket_pack<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(slots, chunks, chunk_pos,
+  launch_k(k_bucket_pack, chunk_grid(n_chunks), 256, 0, as_stream(stream), slots, chunks, chunk_pos,
                                                                     n_chunks, bucket);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
@@ -323,7 +337,7 @@ int nnl_bucket_unpack_mean(const nnl_param_slot* slots, const nnl_chunk* chunks,
                            const int64_t* chunk_pos, int32_t n_chunks, const float* bucket,
                            int32_t world, int32_t* nonfinite, void* stream) {
   if (n_chunks <= 0) return NNL_OK;
-  k_bucket_unpack<<<chunk_grid(n_chunks), 256, 0, as_stream(stream)>>>(
+  launch_k(k_bucket_unpack, chunk_grid(n_chunks), 256, 0, as_stream(stream), 
       slots, chunks, chunk_pos, n_chunks, bucket, (float)world, nonfinite);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
