@@ -3,7 +3,8 @@
 eager) through torch.profiler/CUPTI: GPU busy time, idle gaps between
 consecutive kernels, and the kernels with the largest total time.
 
-    python tools/gap_profile.py [--batch 256] [--steps 3] [--no-graph]
+    python tools/gap_profile.py [--config resnet50|resnet18|lenet|mlp] [--batch B]
+                                [--steps 3] [--no-graph] [--full-names]
 """
 import argparse
 import collections
@@ -17,7 +18,10 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--config", default="resnet50")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--full-names", action="store_true")
+    ap.add_argument("--list", action="store_true", help="every launch of the last step, in order")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
@@ -29,20 +33,17 @@ def main():
     import paper_2102_06725_b200.functions as F
     from paper_2102_06725_b200 import networks
     from paper_2102_06725_b200.communicator import DataParallelTrainer
-    nn.set_default_context(nn.ExecutionContext(type_config=nn.TypeConfig.HALF))
-    B = args.batch
-
-    def build(bs):
-        xv = nn.Variable((bs, 3, 224, 224))
-        tv = nn.Variable((bs,))
-        return {"x": xv, "label": tv,
-                "loss": F.softmax_cross_entropy(networks.resnet50(xv, 1000), tv)}
-
-    tr = DataParallelTrainer(1, B, build, lr=0.1, seed=0,
-                             loss_scaling=nn.DynamicLossScaler(8.0, 2.0, 2000),
-                             check_sync=False, momentum=0.9, weight_decay=1e-4)
-    x = nn.RngState(1).next_uniform_device((B, 3, 224, 224), 0.0, 1.0).cpu().numpy()
-    lab = (np.arange(B) % 1000).astype(np.float32)
+    import bench
+    cf = bench.CONFIGS[args.config]
+    tc = nn.TypeConfig.HALF if cf["half"] else nn.TypeConfig.FLOAT
+    nn.set_default_context(nn.ExecutionContext(type_config=tc))
+    B = args.batch or cf["batch"]
+    scaler = nn.DynamicLossScaler(*cf["scaler"]) if cf["scaler"] else None
+    tr = DataParallelTrainer(1, B, lambda bs: bench.build_graph(nn, F, networks, args.config, bs),
+                             lr=cf["lr"], seed=0, loss_scaling=scaler, check_sync=False,
+                             momentum=cf["momentum"], weight_decay=cf["wd"])
+    x = nn.RngState(1).next_uniform_device((B,) + cf["shape"], 0.0, 1.0).cpu().numpy()
+    lab = (np.arange(B) % cf["classes"]).astype(np.float32)
     for _ in range(3):
         tr.step(x, lab)
     if not args.no_graph:
@@ -66,12 +67,16 @@ def main():
     print(f"steps {args.steps}: kernels {len(ks)}, wall {wall / 1e3 / args.steps:.3f} ms/step, "
           f"busy {busy / 1e3 / args.steps:.3f} ms/step, gaps {sum(gaps) / 1e3 / args.steps:.3f} "
           f"ms/step (median gap {sorted(gaps)[len(gaps) // 2]:.2f} us)")
+    if args.list:
+        per = len(ks) // args.steps
+        for a, b, n in ks[-per:]:
+            print(f"{(b - a):9.2f} us  {n[:150]}")
     agg = collections.defaultdict(lambda: [0, 0.0])
     for a, b, n in ks:
-        k = re.sub(r"<.*", "", re.sub(r"\(.*", "", n)).replace("void ", "")
+        k = n if args.full_names else re.sub(r"<.*", "", re.sub(r"\(.*", "", n)).replace("void ", "")
         agg[k][0] += 1
         agg[k][1] += (b - a)
-    for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:20]:
+    for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:30]:
         print(f"{t / 1e3 / args.steps:8.3f} ms/step {n // args.steps:5d}  {k}")
 
 
