@@ -121,18 +121,60 @@ def peaks() -> dict:
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock and throttle-reason sampling during the timed region
+    (B200_PROFILING.md's clocks line).  In-process NVML in a background thread
+    every 2 ms, so even a sub-millisecond timed region (the C1/C2 latency
+    configs) is sampled; nvidia-smi -lms 100 when NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits (nvml.h)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.thread = None
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.nvml = None
         self.path = tempfile.mktemp(suffix=".csv")
 
+    def sample_now(self):
+        """One synchronous sample: called inside the timed region after the
+        steps are queued, while the GPU is still executing them."""
+        if self.nvml is None:
+            return
+        try:
+            n, h = self.nvml, self.handle
+            self.samples.append((float(n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)),
+                                 float(n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)),
+                                 int(n.nvmlDeviceGetCurrentClocksEventReasons(h))))
+        except Exception:  # noqa: BLE001 -- sampling must never break the bench
+            pass
+
+    def _nvml_loop(self, stop):
+        while not stop.is_set():
+            self.sample_now()
+            stop.wait(0.002)
+
     def __enter__(self):
+        import threading
+        try:
+            import pynvml as nvml
+            nvml.nvmlInit()
+            self.handle = nvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = nvml
+            self.stop = threading.Event()
+            # a short GIL switch interval lets the sampler run inside sub-ms regions
+            self.switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)
+            self.thread = threading.Thread(target=self._nvml_loop, args=(self.stop,), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.thread = None
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -143,6 +185,10 @@ class Clocks:
         return self
 
     def __exit__(self, *exc):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join()
+            sys.setswitchinterval(self.switch)
         if self.proc is not None:
             self.proc.terminate()
             self.proc.wait()
@@ -150,6 +196,10 @@ class Clocks:
 
     def summary(self) -> dict:
         sm, mx, reasons = [], [], set()
+        for s_mhz, m_mhz, bits in self.samples:
+            sm.append(s_mhz)
+            mx.append(m_mhz)
+            reasons.update(k for k, v in self.BITS.items() if bits & v)
         try:
             for line in open(self.path):
                 parts = [p.strip() for p in line.split(",")]
@@ -170,7 +220,8 @@ class Clocks:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def _oracle_builder(name):
@@ -348,6 +399,12 @@ def main():
         for _ in range(K):
             trainer.step_resident()
         e.record()
+        # the queued steps are still running: sample the clocks while polling
+        # for their end (NVML queries are ~10 us; the device events time the steps)
+        clk.sample_now()
+        while not e.query():
+            clk.sample_now()
+            time.sleep(0.001)
         sync()
         ms = max_over_ranks(s.elapsed_time(e))
     launches = int(_lib.lib().nnl_launch_count(1))

@@ -85,6 +85,13 @@ bool tc_eligible(const GemmProblem& pb, int dtype);
 int32_t tc_stat_rows(const GemmProblem& pb, int dtype);
 // partial rows of a dgrad with fused BN-backward statistics (0: unsupported)
 int32_t tc_bnb_rows(const GemmProblem& pb, int dtype);
+// 3x3 / stride-1 weight gradients with shared halos (gemm_wgrad3.cu)
+bool wgrad3_eligible(const GemmProblem& pb, int dtype);
+size_t wgrad3_ws_bytes(const GemmProblem& pb);
+int wgrad3_run(const GemmProblem& pb, void* ws, size_t ws_bytes, cudaStream_t st);
+// out[m*ldc + n] = q(prev + sum_s partial[s][m][n]) in fixed split order (gemm_tc.cu)
+int tc_splitk_reduce(int M, int N, int splits, const float* partial, __half* out, int64_t ldc,
+                     int acc, int32_t* nonfinite, cudaStream_t st);
 // column sums of dy (bias gradient, functions.py:116,212): db[n] = q(prev + sum_m dy[m][n])
 int bias_grad(int dtype, int64_t rows, int64_t cols, const void* dy, void* db, int acc,
               int32_t* nonfinite, void* ws, size_t ws_bytes, cudaStream_t st);

@@ -2246,6 +2246,7 @@ bool tc_eligible(const GemmProblem& pb, int dtype) {
 size_t tc_ws_bytes(const GemmProblem& pb) {
   Plan pl = make_plan(pb);
   if (!pl.ok) return 0;
+  if (wgrad3_eligible(pb, NNL_F16)) return wgrad3_ws_bytes(pb) + 4 * 256;
   size_t w = pl.ws_im2col + pl.ws_wpad + pl.ws_partial + pl.ws_x4 + pl.ws_xs;
   for (int cls = 1; cls < pl.nclass; ++cls) {
     Plan q = make_plan(pb, cls);
@@ -2286,8 +2287,18 @@ static inline uint8_t* align256(uint8_t* p) {
 
 static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st);
 
+int tc_splitk_reduce(int M, int N, int splits, const float* partial, __half* out, int64_t ldc,
+                     int acc, int32_t* nonfinite, cudaStream_t st) {
+  if (N % 4 || ldc % 4) return fail(NNL_ERR_INVALID_ARGUMENT, "split reduction needs N % 4 == 0");
+  launch_k(k_tc_splitk_reduce4, grid_for((int64_t)M * N / 4, 256), 256, 0, st, M, N, splits,
+           partial, (const __half*)nullptr, out, ldc, acc, nonfinite);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
 int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (dtype != NNL_F16) return NNL_ERR_UNSUPPORTED;
+  if (wgrad3_eligible(pb, dtype)) return wgrad3_run(pb, ws, ws_bytes, st);
   Plan p0 = make_plan(pb, 0);
   if (!p0.ok) return NNL_ERR_UNSUPPORTED;
   if (ws_bytes < tc_ws_bytes(pb)) return fail(NNL_ERR_INVALID_ARGUMENT, "tc workspace too small");

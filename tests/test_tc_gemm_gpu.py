@@ -32,6 +32,10 @@ CONV = [  # (B, cin, cout, k, stride, pad, hw)
     (2, 64, 64, 3, 1, 1, 56),      # shared-halo tiles at the ResNet-50 stage-1 extent
     (4, 64, 128, 3, 2, 1, 16),     # strided 3x3 dgrad: 4 parity-class GEMMs
     (2, 64, 64, 3, 1, 0, 9),       # valid (pad 0) 3x3: dgrad im2col bounding box
+    (2, 128, 64, 3, 1, 1, 14),     # halo wgrad: 14x14 maps in 2x2 8x8 tiles, two channel blocks
+    (3, 64, 192, 3, 1, 1, 17),     # halo wgrad: three output blocks, ragged 17x17 tiles
+    (2, 512, 512, 3, 1, 1, 14),    # halo wgrad: 64 block pairs
+    (2, 512, 512, 3, 1, 1, 7),     # 7x7 maps: the per-tap im2col wgrad
 ]
 
 
