@@ -24,6 +24,8 @@
 // partials reduced in fixed order afterwards.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "gemm.cuh"
 #include "tc_ptx.cuh"
 
@@ -1216,51 +1218,91 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 #ifndef NNL_TC_INSTANTIATE  // helper kernels: host-side TU only
-// out = q(prev + bias + sum_s partial[s][m][n]), fixed split order; `trans`
-// writes D[m][n] to out[n*ldc + m]
-// the same reduction, 4 consecutive columns per thread (plain layout, N and ldc
-// multiples of 4): float4 partial loads in the same split order, 8 B stores
-__global__ void k_tc_splitk_reduce4(int M, int N, int splits, const float* __restrict__ partial,
-                                    const __half* __restrict__ bias, __half* __restrict__ out,
-                                    int64_t ldc, int acc, int32_t* nonfinite) {
+// out = q(prev + bias + sum_s partial[s][m][n]), 4 consecutive columns per
+// thread (plain layout, N and ldc multiples of 4), float4 partial loads, 8 B
+// stores.  P split groups per float4 column: thread group g sums splits g, g + P, ...
+// in ascending order and the P group sums are added in ascending g -- a fixed
+// association (deterministic, independent of the grid), with P loads in
+// flight per output instead of one chain of `splits` dependent loads
+template <int P>
+__global__ void __launch_bounds__(256) k_tc_splitk_reduce4(
+    int M, int N, int splits, const float* __restrict__ partial, const __half* __restrict__ bias,
+    __half* __restrict__ out, int64_t ldc, int acc, int32_t* nonfinite) {
   pdl_wait();
   pdl_trigger();
-  int bad = 0;
+  constexpr int COLS = 256 / P;
+  __shared__ float4 red[P][COLS];
+  const int g = threadIdx.x / COLS, cl = threadIdx.x % COLS;
   const int64_t total = (int64_t)M * N, total4 = total / 4;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total4;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = 4 * t;
-    const int64_t m = i / N, n = i % N;
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int z = 0; z < splits; ++z) {
-      const float4 p = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + i);
+  const int64_t t = (int64_t)blockIdx.x * COLS + cl;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t < total4) {
+#pragma unroll 4
+    for (int z = g; z < splits; z += P) {
+      const float4 p = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + 4 * t);
       s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
     }
+  }
+  if (P > 1) {
+    red[g][cl] = s;
+    __syncthreads();
+  }
+  int bad = 0;
+  if (g == 0 && t < total4) {
+    if (P > 1) {
+      s = red[0][cl];
+#pragma unroll
+      for (int q = 1; q < P; ++q) {
+        const float4 r = red[q][cl];
+        s.x += r.x; s.y += r.y; s.z += r.z; s.w += r.w;
+      }
+    }
+    const int64_t i = 4 * t;
+    const int64_t m = i / N, n = i % N;
     float v[4] = {s.x, s.y, s.z, s.w};
     if (bias) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) v[e] = __fadd_rn(v[e], __half2float(bias[n + e]));
     }
     uint2* o = reinterpret_cast<uint2*>(out + m * ldc + n);
-    float p[4] = {0.f, 0.f, 0.f, 0.f};
+    float pv[4] = {0.f, 0.f, 0.f, 0.f};
     if (acc) {
       const uint2 u = *o;
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
-      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
-      p[0] = a.x; p[1] = a.y; p[2] = b.x; p[3] = b.y;
+      const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+      const float2 b0 = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+      pv[0] = a0.x; pv[1] = a0.y; pv[2] = b0.x; pv[3] = b0.y;
     }
-    const __half2 h0 = __floats2half2_rn(__fadd_rn(p[0], v[0]), __fadd_rn(p[1], v[1]));
-    const __half2 h1 = __floats2half2_rn(__fadd_rn(p[2], v[2]), __fadd_rn(p[3], v[3]));
+    const __half2 h0 = __floats2half2_rn(__fadd_rn(pv[0], v[0]), __fadd_rn(pv[1], v[1]));
+    const __half2 h1 = __floats2half2_rn(__fadd_rn(pv[2], v[2]), __fadd_rn(pv[3], v[3]));
     uint2 w;
     w.x = *reinterpret_cast<const uint32_t*>(&h0);
     w.y = *reinterpret_cast<const uint32_t*>(&h1);
     *o = w;
     const float2 c0 = __half22float2(h0), c1 = __half22float2(h1);
-    bad |= !isfinite(c0.x) | !isfinite(c0.y) | !isfinite(c1.x) | !isfinite(c1.y);
+    bad = !isfinite(c0.x) | !isfinite(c0.y) | !isfinite(c1.x) | !isfinite(c1.y);
   }
   if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
 }
 
+// launch the grouped reduction: 8 groups once there are >= 16 splits
+static int launch_reduce4(int M, int N, int splits, const float* partial, const __half* bias,
+                          __half* out, int64_t ldc, int acc, int32_t* nonfinite, cudaStream_t st) {
+  const int64_t total4 = (int64_t)M * N / 4;
+  if (splits >= 16)
+    launch_k(k_tc_splitk_reduce4<8>, (unsigned)((total4 + 31) / 32), 256, 0, st, M, N, splits,
+             partial, bias, out, ldc, acc, nonfinite);
+  else if (splits >= 4)
+    launch_k(k_tc_splitk_reduce4<4>, (unsigned)((total4 + 63) / 64), 256, 0, st, M, N, splits,
+             partial, bias, out, ldc, acc, nonfinite);
+  else
+    launch_k(k_tc_splitk_reduce4<1>, (unsigned)((total4 + 255) / 256), 256, 0, st, M, N, splits,
+             partial, bias, out, ldc, acc, nonfinite);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+// the general form: one column per thread, fixed split order; `trans` writes
+// D[m][n] to out[n*ldc + m]
 __global__ void k_tc_splitk_reduce(int M, int N, int splits, const float* __restrict__ partial,
                                    const __half* __restrict__ bias, __half* __restrict__ out,
                                    int64_t ldc, int acc, int trans, int c4, int c4_s2,
@@ -2043,6 +2085,14 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   }
   if (pl.bmode == B_TMA_MN && pl.b_kblk == 0) pl.b_kblk = 1 << 30;
   pl.bn = pick_bn(pl, pl.bmode == B_TMA_MN && pl.b_tap_stride && !k1);
+  // weight gradients (long, splittable reductions) with more than 128 output
+  // channels: 256 x 256 CTA-pair tiles move the fewest operand bytes per FLOP
+  // through L2 -> SMEM (the mainloop bound; measured 0-25 % faster per layer,
+  // slower for single-CTA 128-row tiles).  NNL_WG_BN=128 restores the cost model.
+  static const int wg_bn = getenv("NNL_WG_BN") ? atoi(getenv("NNL_WG_BN")) : 256;
+  if (pb.mode == kWgrad && !pb.g.affine && pl.N > 128 && pl.M > BM && !pl.c4 && !pl.s2d &&
+      pl.bmode != B_GATHER_WGRAD && wg_bn == 256)
+    pl.bn = 256;
   if (pb.bnx && pl.bn > 128) pl.bn = 128;  // the fused BN-backward epilogue's smem budget
   if (pl.remap && pl.N % pl.bn) pl.bn = 64;
   pl.num_kb = pl.halo ? 1 : (int)cdiv(pl.K, BK);  // A_HALO: one ring stage per tile
@@ -2087,9 +2137,12 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
                        pl.amode == A_TILE4 || pl.amode == A_TILE4MN;
     const bool b_tma = pl.bmode == B_TMA_K || pl.bmode == B_TMA_MN || pl.bmode == B_IM2COL ||
                        pl.bmode == B_TILE4;
+    // weight gradients always pair (measured: every ResNet-50 wgrad with
+    // M > 128 output channels, 5-20 % faster; forward/dgrad tiles only when wide and long)
     const int pol = cta_pair_policy();
+    const bool wg = pb.mode == kWgrad && !pb.g.affine;
     if (pol && a_tma && b_tma && pl.bn >= 128 && pl.M > BM && !pb.bnx &&
-        (pol == 2 || (pl.bn == 256 && pl.kb_per_split >= 16)))
+        (pol == 2 || wg || (pl.bn == 256 && pl.kb_per_split >= 16)))
       tile_and_split(2);
   }
   {
@@ -2290,10 +2343,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st);
 int tc_splitk_reduce(int M, int N, int splits, const float* partial, __half* out, int64_t ldc,
                      int acc, int32_t* nonfinite, cudaStream_t st) {
   if (N % 4 || ldc % 4) return fail(NNL_ERR_INVALID_ARGUMENT, "split reduction needs N % 4 == 0");
-  launch_k(k_tc_splitk_reduce4, grid_for((int64_t)M * N / 4, 256), 256, 0, st, M, N, splits,
-           partial, (const __half*)nullptr, out, ldc, acc, nonfinite);
-  NNL_CHECK_LAUNCH();
-  return NNL_OK;
+  return launch_reduce4(M, N, splits, partial, nullptr, out, ldc, acc, nonfinite, st);
 }
 
 int tc_gemm(const GemmProblem& pb, int dtype, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -2531,9 +2581,9 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     const int c4 = mapped ? g.c : 0;
     if (!mapped && pl.N % 4 == 0 && pl.ldc % 4 == 0 &&
         !(reinterpret_cast<uintptr_t>(pb.out) & 7))
-      launch_k(k_tc_splitk_reduce4, grid_for((int64_t)pl.M * pl.N / 4, 256), 256, 0, st, 
-          pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),
-          reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, pb.nonfinite);
+      return launch_reduce4(pl.M, pl.N, pl.splits, partial,
+                            reinterpret_cast<const __half*>(pb.bias),
+                            reinterpret_cast<__half*>(pb.out), pl.ldc, pb.acc, pb.nonfinite, st);
     else
       launch_k(k_tc_splitk_reduce, grid_for((int64_t)pl.M * pl.N, 256), 256, 0, st, 
           pl.M, pl.N, pl.splits, partial, reinterpret_cast<const __half*>(pb.bias),

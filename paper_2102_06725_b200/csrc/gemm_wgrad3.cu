@@ -56,6 +56,7 @@ struct W3Args {
   __half* out;           // dW [k][3][3][c]
   int acc;
   int32_t* nonfinite;
+  int dbg;               // probes (NNL_WG3_DBG): 1 = no MMAs, 2 = no operand loads
 };
 
 __device__ __forceinline__ void decode(const W3Args& a, int u, int& cb, int& nb, int& sp) {
@@ -111,6 +112,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = t0; t < t1; ++t, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          if (a.dbg & 2) {
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_arrive_tx(&full[s], kHaloBytes + kDyBytes);
           const int img = t / per_img, r = t - img * per_img;
           const int ty = r / a.tw, tx = r - ty * a.tw;
@@ -125,6 +130,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t IDESC = idesc_f16(64, true, true, 128);
+    // all 24 descriptors of stage 0 built once (the issuing thread is otherwise
+    // the bottleneck: ~10 integer ops per descriptor against a 48-cycle MMA);
+    // stage s adds s * kStageBytes / 16 to the start-address field (< 2^14)
+    const uint32_t base0 = smem_u32(smem);
+    uint64_t dA[kMT][4], dB[4];
+#pragma unroll
+    for (int j = 0; j < kMT; ++j) {
+      const int ta = 2 * j, tb = 2 * j + 1 < 9 ? 2 * j + 1 : 2 * j;
+      const uint32_t oa = (uint32_t)(((ta / 3) * kPitch + ta % 3) * 128);
+      const uint32_t ob = (uint32_t)(((tb / 3) * kPitch + tb % 3) * 128);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)  // 16 pixels = tile rows 2kk, 2kk + 1
+        dA[j][kk] = sdesc_sw128(base0 + oa + (uint32_t)(kk * 2 * kPitch * 128), ob - oa,
+                                kPitch * 128);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      dB[kk] = sdesc_sw128(base0 + kHaloStage + (uint32_t)(kk * 2048), 8192, 1024);
     int it = 0, ut = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++ut) {
       int cb, nb, sp;
@@ -136,22 +159,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = it % kStages;
         mbar_wait(&full[s], (it / kStages) & 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t hb = smem_u32(smem + s * kStageBytes);
-          const uint32_t db = hb + kHaloStage;
+        if (a.dbg == 1) {
+          if (elect_one()) mbar_arrive(&empty[s]);
+        } else if (elect_one()) {
+          const uint64_t so = (uint64_t)((uint32_t)(s * kStageBytes) >> 4);
+          const uint32_t acc0 = t > t0 ? 1u : 0u;
 #pragma unroll
-          for (int j = 0; j < kMT; ++j) {
-            const int ta = 2 * j, tb = 2 * j + 1 < 9 ? 2 * j + 1 : 2 * j;
-            const uint32_t oa = (uint32_t)(((ta / 3) * kPitch + ta % 3) * 128);
-            const uint32_t ob = (uint32_t)(((tb / 3) * kPitch + tb % 3) * 128);
+          for (int j = 0; j < kMT; ++j)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {  // 16 pixels = tile rows 2kk, 2kk + 1
-              const uint64_t da =
-                  sdesc_sw128(hb + oa + (uint32_t)(kk * 2 * kPitch * 128), ob - oa, kPitch * 128);
-              const uint64_t dbd = sdesc_sw128(db + (uint32_t)(kk * 2048), 8192, 1024);
-              mma_f16(tmem + (uint32_t)(j * 64), da, dbd, IDESC, (t > t0 || kk > 0) ? 1u : 0u);
-            }
-          }
+            for (int kk = 0; kk < 4; ++kk)
+              mma_f16(tmem + (uint32_t)(j * 64), dA[j][kk] + so, dB[kk] + so, IDESC,
+                      kk ? 1u : acc0);
           mma_commit(&empty[s]);
         }
         __syncwarp();
@@ -330,6 +348,8 @@ int wgrad3_run(const GemmProblem& pb, void* ws, size_t ws_bytes, cudaStream_t st
   a.out = reinterpret_cast<__half*>(pb.out);
   a.acc = pb.acc;
   a.nonfinite = p.splits > 1 ? nullptr : pb.nonfinite;
+  static const int dbg = getenv("NNL_WG3_DBG") ? atoi(getenv("NNL_WG3_DBG")) : 0;
+  a.dbg = dbg;
   static bool attr = false;
   if (!attr) {
     NNL_CUDA(cudaFuncSetAttribute(k_tc_wgrad3, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
