@@ -330,6 +330,65 @@ def gen_nnp(nn, networks):
     return out
 
 
+# operator-protocol cases for the reference-side binding (nanonnl_plugin): the
+# reference's own FunctionImpl classes driven exactly as its engine drives them
+# (infer_shapes, forward(node, xs), backward(node, gys, want)), float32, with a
+# random upstream gradient
+PLUGIN_CASES = [
+    ("affine", "Affine", {}, [(4, 3, 5), (15, 6), (6,)]),
+    ("conv", "Convolution", {"stride": (2, 2), "pad": (1, 1), "kernel": (3, 3)},
+     [(2, 3, 9, 9), (4, 3, 3, 3), (4,)]),
+    ("pool", "MaxPooling", {"kernel": (3, 3), "stride": (2, 2), "pad": (1, 1)}, [(2, 3, 7, 7)]),
+    ("relu", "ReLU", {}, [(3, 10)]),
+    ("sce", "SoftmaxCrossEntropy", {}, [(5, 7), (5,)]),
+    ("bn", "BatchNormalization", {"eps": 1e-5, "momentum": 0.9, "batch_stat": True},
+     [(4, 3, 5, 5), (3,), (3,), (3,), (3,)]),
+]
+
+
+def gen_plugin(nn):
+    from types import SimpleNamespace
+
+    import nanonnl.functions as RF
+    from nanonnl.tensor import RngState
+    rng = RngState(seed=21)
+    fresh(nn, False)
+    out = {}
+    for name, kind, args, shapes in PLUGIN_CASES:
+        xs = [rng.next_uniform(s, -1.0, 1.0) for s in shapes]
+        if kind == "SoftmaxCrossEntropy":
+            xs[1] = (np.arange(shapes[1][0]) * 3 % shapes[0][1]).astype(np.float32)
+        if kind == "BatchNormalization":
+            xs[1] = rng.next_uniform(shapes[1], 0.5, 1.5)
+            xs[4] = rng.next_uniform(shapes[4], 0.5, 1.5)
+        if kind == "MaxPooling":
+            xs[0] = np.round(xs[0] * 4) / 4  # ties: first max wins
+        vs = []
+        for i, a in enumerate(xs):
+            v = nn.Variable(a.shape, need_grad=not (kind == "SoftmaxCrossEntropy" and i == 1))
+            v.d = a
+            vs.append(v)
+        impl = RF.REGISTRY[kind](**args)
+        ys_shapes = impl.infer_shapes([v.shape for v in vs])
+        node = SimpleNamespace(inputs=vs, state={})
+        ys = impl.forward(node, [v.data.values for v in vs])
+        gys = [rng.next_uniform(s, -1.0, 1.0) for s in ys_shapes]
+        want = [v.need_grad for v in vs]
+        gxs = impl.backward(node, gys, want)
+        for i, a in enumerate(xs):
+            out[f"{name}__x{i}"] = a
+        for j, (y, gy) in enumerate(zip(ys, gys)):
+            out[f"{name}__y{j}"] = np.asarray(y, np.float32)
+            out[f"{name}__gy{j}"] = gy
+        for i, g in enumerate(gxs):
+            if g is not None:
+                out[f"{name}__g{i}"] = np.asarray(g, np.float32)
+        if kind == "BatchNormalization":
+            out[f"{name}__mean"] = vs[3].d.copy()
+            out[f"{name}__var"] = vs[4].d.copy()
+    return out
+
+
 def main():
     nn, F, PF, networks, DPT = _ref()
     np.savez_compressed(os.path.join(HERE, "nnp.npz"), **gen_nnp(nn, networks))
@@ -338,6 +397,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "solver.npz"), **gen_solver(nn))
     np.savez_compressed(os.path.join(HERE, "lenet.npz"), **gen_lenet(nn, networks, DPT))
     np.savez_compressed(os.path.join(HERE, "mlp.npz"), **gen_mlp(nn, networks))
+    np.savez_compressed(os.path.join(HERE, "plugin.npz"), **gen_plugin(nn))
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
