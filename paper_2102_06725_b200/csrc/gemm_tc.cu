@@ -70,7 +70,7 @@ constexpr int BM = 128, BK = 64, kThreads = 384;
 // RB = 1: the whole B operand (all k-blocks of a single-N-tile GEMM, <= RES_MAX
 // bytes) stays resident in shared memory for the CTA's lifetime; the ring then
 // streams A only (weight-stationary narrow convolutions).
-constexpr int RES_MAX = 96 * 1024;
+constexpr int RES_MAX = 64 * 1024;
 
 // EP = 1 (fused BN-backward epilogue): each of the 8 epilogue warps keeps two
 // 6 KB sets of TMA-loaded input tiles (x, gate, prev: 32 rows x 32 columns each)
@@ -86,7 +86,7 @@ struct Cfg {
   static constexpr int MAX_STAT_N = HL ? 64 : 2048;  // per-CTA BN statistics [2][N]
   static constexpr int STAT_BYTES = 2 * MAX_STAT_N * 4;
   // TMA-store staging: 8 x 4 KB (4 warps x 2 buffers, or 8 warps x 1)
-  static constexpr int STG_BYTES = EP ? 8 * 2 * 6144 : 4 * 2 * 4096;
+  static constexpr int STG_BYTES = EP ? 8 * 2 * 6144 : (RB ? 8 * 2 * 4096 : 4 * 2 * 4096);
   static constexpr int FIXED =
       1024 + RED_BYTES + BIAS_BYTES + STAT_BYTES + STG_BYTES + 1024 + RES_BYTES;
   static constexpr int BUDGET = 232448;
@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TMA-fed tiles leave warps 4..7 free: they join the epilogue
   constexpr bool kEpi8 = !kGA && !kGB;
   constexpr int kEpi = kEpi8 ? 8 : 4, kEpiWarp0 = kEpi8 ? 4 : 8;
-  constexpr int kStgBufs = kEpi8 ? 1 : 2;  // 4 KB TMA-store staging buffers per warp
+  // 4 KB TMA-store staging buffers per warp: two (store i drains while chunk
+  // i + 1 is rounded) except for 8-warp epilogues of streamed-B tiles
+  constexpr int kStgBufs = (kEpi8 && !RB) ? 1 : 2;
   // TMA-store chunk width: 64 columns (128 B rows, 128 B swizzle), or 32 (64 B
   // rows, 64 B swizzle) when eight warps share a 64-wide tile
   constexpr int CW = (kEpi8 && BN == 64) ? 32 : 64;
