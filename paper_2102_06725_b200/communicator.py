@@ -712,6 +712,8 @@ class DataParallelTrainer:
         t.cuda.current_stream().wait_stream(side)
         self.graph_kernels = int(_lib.lib().nnl_launch_count(0) - before)  # libnnl kernels/step
         self._graph = g
+        if getattr(self, "_feed", None) is not None:
+            self._feed["graphs"] = [None, None]  # step_async re-records its I/O graphs
 
     def step_resident(self) -> None:
         """One step on the inputs already resident on the device: no host
@@ -755,7 +757,10 @@ class DataParallelTrainer:
         Same math as `step`: the device-side work of a step starts with the
         import of its inputs and ends with the loss read-back.  Pass pinned host
         arrays (e.g. `torch.empty(..., pin_memory=True).numpy()`) for an
-        asynchronous copy."""
+        asynchronous copy.  After `capture_graph()`, each staging slot gets its
+        own graph holding the input imports, the step and the loss export, so a
+        step costs the host two copies, one replay and a read-back (the events
+        and pinned loss slots are allocated once)."""
         if self.distributed or self.n_workers != 1:
             raise NotImplementedError("step_async is implemented for one replica per process")
         t = _lib.torch()
@@ -768,9 +773,16 @@ class DataParallelTrainer:
                 "stream": t.cuda.Stream(),
                 "x": [t.empty(xv.shape, dtype=t.float32, device=dev) for _ in range(2)],
                 "t": [t.empty(lv.shape, dtype=t.float32, device=dev) for _ in range(2)],
-                "free": [None, None],   # event: the slot's import has consumed it
+                "free": [t.cuda.Event() for _ in range(2)],   # slot's import consumed it
+                "used": [False, False],
+                "copied": [t.cuda.Event() for _ in range(2)],
                 "slot": 0,
                 "loss_dev": t.empty(1, dtype=t.float32, device=dev),
+                # pinned loss slots + their events, reused round robin
+                "host": [t.empty(1, dtype=t.float32, pin_memory=True) for _ in range(8)],
+                "done": [t.cuda.Event() for _ in range(8)],
+                "ring": 0,
+                "graphs": [None, None],
             }
         x = np.asarray(x_batch, dtype=np.float32)[:self.shard_size]
         lab = np.asarray(label_batch, dtype=np.float32)[:self.shard_size]
@@ -781,33 +793,57 @@ class DataParallelTrainer:
         feed["slot"] ^= 1
         cs, main = feed["stream"], t.cuda.current_stream()
         with t.cuda.stream(cs):
-            if feed["free"][slot] is not None:
+            if feed["used"][slot]:
                 cs.wait_event(feed["free"][slot])
             hx, hl = t.from_numpy(np.ascontiguousarray(x)), t.from_numpy(np.ascontiguousarray(lab))
             feed["x"][slot].copy_(hx, non_blocking=hx.is_pinned())
             feed["t"][slot].copy_(hl, non_blocking=hl.is_pinned())
-            copied = t.cuda.Event()
-            copied.record(cs)
-        main.wait_event(copied)
-        xv.data.write_f32_device(feed["x"][slot])
-        lv.data.write_f32_device(feed["t"][slot])
-        free = t.cuda.Event()
-        free.record(main)
-        feed["free"][slot] = free
+            feed["copied"][slot].record(cs)
+        main.wait_event(feed["copied"][slot])
         graph = getattr(self, "_graph", None)
         if graph is not None:
             self._check_labels(rep)
-            graph.replay()
-            loss = rep.handles["loss"]
+            io = feed["graphs"][slot]
+            if io is None:
+                io = feed["graphs"][slot] = self._capture_io(rep, feed, slot)
+            io.replay()
         else:
-            loss = self._work(rep, 0, None, None, lambda r: None)
-        _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr,
-                  feed["loss_dev"].data_ptr(), _lib.stream())
-        host = t.empty(1, dtype=t.float32, pin_memory=True)  # one per pending step
+            self._import_and_export(rep, feed, slot, lambda: self._work(rep, 0, None, None,
+                                                                          lambda r: None))
+        feed["free"][slot].record(main)
+        feed["used"][slot] = True
+        k = feed["ring"]
+        feed["ring"] = (k + 1) % len(feed["host"])
+        host = feed["host"][k]
         host.copy_(feed["loss_dev"], non_blocking=True)
-        done = t.cuda.Event()
+        done = feed["done"][k]
         done.record(main)
         return PendingLoss(done, host)
+
+    def _import_and_export(self, rep, feed, slot, body) -> None:
+        """The device part of one `step_async` step: import the staging slot's
+        inputs, run `body` (the step), export the loss to `feed["loss_dev"]`."""
+        rep.handles["x"].data.write_f32_device(feed["x"][slot])
+        rep.handles["label"].data.write_f32_device(feed["t"][slot])
+        body()
+        loss = rep.handles["loss"]
+        _lib.call("nnl_export_f32", loss.data.code, 1, 1, 1, loss.data.ptr,
+                  feed["loss_dev"].data_ptr(), _lib.stream())
+
+    def _capture_io(self, rep, feed, slot):
+        """CUDA graph of `_import_and_export` for one staging slot (the step body
+        recorded the same way as `capture_graph`)."""
+        t = _lib.torch()
+        side = t.cuda.Stream()
+        side.wait_stream(t.cuda.current_stream())
+        body = lambda: self._work(rep, 0, None, None, lambda r: None)  # noqa: E731
+        # no warm-up run: capture_graph() already ran this step body, so every
+        # buffer and workspace exists; recording executes nothing
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g, stream=side):
+            self._import_and_export(rep, feed, slot, body)
+        t.cuda.current_stream().wait_stream(side)
+        return g
 
     def step(self, x_batch: np.ndarray, label_batch: np.ndarray, shard: bool = False) -> float:
         """One synchronised step; returns the batch loss (mean of shard losses).

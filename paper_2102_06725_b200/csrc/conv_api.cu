@@ -42,12 +42,53 @@ static GemmProblem conv_problem(const nnl_conv_shape* cs, int mode) {
   return pb;
 }
 
+// Stride-1 dgrad as a forward convolution (functions.py:208-209 restated):
+// dx = conv(dy, W') with W'[c][r][s][k] = W[k][R-1-r][S-1-s][c] and padding
+// R-1-p, so narrow output-channel layers (LeNet's conv2, K = 16) whose dgrad
+// the tcgen05 plans do not take run on the forward path's tensor cores
+// instead of the SIMT kernel.  Same sums per output (reduction order aside).
+static bool dgrad_as_fprop(const nnl_conv_shape* cs, int dtype, GemmProblem& q) {
+  if (dtype != NNL_F16 || !g_tc_enabled || cs->stride_h != 1 || cs->stride_w != 1 ||
+      cs->pad_h > cs->r - 1 || cs->pad_w > cs->s - 1)
+    return false;
+  if (tc_eligible(conv_problem(cs, kDgrad), dtype)) return false;
+  nnl_conv_shape f = *cs;
+  f.h = cs->p; f.w = cs->q; f.c = cs->k; f.k = cs->c;
+  f.pad_h = cs->r - 1 - cs->pad_h; f.pad_w = cs->s - 1 - cs->pad_w;
+  f.p = cs->h; f.q = cs->w;
+  q = conv_problem(&f, kFprop);
+  return tc_eligible(q, dtype);
+}
+
+static size_t flip_bytes(const nnl_conv_shape* cs) {
+  return ((size_t)cs->k * cs->c * cs->r * cs->s * 2 + 255) & ~(size_t)255;
+}
+
+__global__ void k_w_flip(int k, int c, int r, int s, const __half* __restrict__ w,
+                         __half* __restrict__ wf) {
+  pdl_wait();
+  pdl_trigger();
+  const int total = k * c * r * s;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    // wf[cc][rr][ss][kk] = w[kk][r-1-rr][s-1-ss][cc]
+    const int kk = i % k, t = i / k;
+    const int ss = t % s, t2 = t / s;
+    const int rr = t2 % r, cc = t2 / r;
+    wf[i] = w[(((int64_t)kk * r + (r - 1 - rr)) * s + (s - 1 - ss)) * c + cc];
+  }
+}
+
 extern "C" {
 
 size_t nnl_conv2d_workspace_size(const nnl_conv_shape* cs, int dtype, int pass) {
   if (check_conv(cs)) return 0;
   GemmProblem pb = conv_problem(cs, pass);
   size_t w = gemm_ws(pb, dtype);
+  GemmProblem q;
+  if (pass == kDgrad && dgrad_as_fprop(cs, dtype, q)) {
+    const size_t f = flip_bytes(cs) + gemm_ws(q, dtype);
+    if (f > w) w = f;
+  }
   if (pass == kWgrad) {
     size_t b = bias_grad_ws_bytes((int64_t)cs->n * cs->p * cs->q, cs->k);
     if (b > w) w = b;
@@ -79,6 +120,18 @@ int nnl_conv2d_bwd_data(const nnl_conv_shape* cs, int dtype, const void* dy, con
   if (rc) return rc;
   GemmProblem pb = conv_problem(cs, kDgrad);
   pb.a = dy; pb.b = w; pb.out = dx; pb.acc = accumulate;
+  GemmProblem q;
+  if (dgrad_as_fprop(cs, dtype, q) && ws_bytes >= flip_bytes(cs) + gemm_ws(q, dtype)) {
+    cudaStream_t st = as_stream(stream);
+    __half* wf = reinterpret_cast<__half*>(ws);
+    const int total = cs->k * cs->c * cs->r * cs->s;
+    launch_k(k_w_flip, grid_for(total, 256), 256, 0, st, cs->k, cs->c, cs->r, cs->s,
+             reinterpret_cast<const __half*>(w), wf);
+    NNL_CHECK_LAUNCH();
+    q.a = dy; q.b = wf; q.out = dx; q.acc = accumulate;
+    return tc_gemm(q, dtype, reinterpret_cast<uint8_t*>(ws) + flip_bytes(cs),
+                   ws_bytes - flip_bytes(cs), st);
+  }
   return run_gemm(pb, dtype, ws, ws_bytes, as_stream(stream));
 }
 

@@ -1514,6 +1514,14 @@ __global__ void k_im2col(ConvGeom g, int M, int kp, const __half* __restrict__ x
     const int k = j * 8;
     int c = k % g.c, t = k / g.c;
     int sx = t % g.s, r = t / g.s;
+    if ((g.c & 7) == 0) {  // the 8 columns are 8 channels of one tap: one 16 B load
+      const int ih = ih0 + r, iw = iw0 + sx;
+      uint4 u = make_uint4(0u, 0u, 0u, 0u);
+      if (k < rsc && (unsigned)ih < (unsigned)g.h && (unsigned)iw < (unsigned)g.w)
+        u = *reinterpret_cast<const uint4*>(xb + (ih * g.w + iw) * g.c + c);
+      *reinterpret_cast<uint4*>(col + (int64_t)m * kp + j * 8) = u;
+      continue;
+    }
     __align__(16) __half v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {

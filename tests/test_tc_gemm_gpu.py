@@ -36,6 +36,8 @@ CONV = [  # (B, cin, cout, k, stride, pad, hw)
     (3, 64, 192, 3, 1, 1, 17),     # halo wgrad: three output blocks, ragged 17x17 tiles
     (2, 512, 512, 3, 1, 1, 14),    # halo wgrad: 64 block pairs
     (2, 512, 512, 3, 1, 1, 7),     # 7x7 maps: the per-tap im2col wgrad
+    (2, 16, 16, 5, 1, 0, 12),      # LeNet conv2: dgrad as a forward conv over flipped weights
+    (3, 16, 32, 3, 1, 1, 9),       # same, padded
 ]
 
 
@@ -44,7 +46,7 @@ def test_conv_backward_accumulate_mode(nnl):
     import paper_2102_06725_b200.functions as F
     _half(nnl)
     for geom in [(2, 64, 128, 1, 2, 0, 8), (2, 64, 64, 3, 1, 1, 8), (2, 128, 256, 1, 1, 0, 6),
-                 (2, 64, 64, 3, 2, 1, 10), (2, 3, 64, 7, 2, 3, 20)]:
+                 (2, 64, 64, 3, 2, 1, 10), (2, 3, 64, 7, 2, 3, 20), (2, 16, 16, 5, 1, 0, 12)]:
         b, cin, cout, k, s, p, hw = geom
         rng = np.random.default_rng(k + cout)
         x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
