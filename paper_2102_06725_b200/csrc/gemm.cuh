@@ -89,6 +89,9 @@ int32_t tc_bnb_rows(const GemmProblem& pb, int dtype);
 bool wgrad3_eligible(const GemmProblem& pb, int dtype);
 size_t wgrad3_ws_bytes(const GemmProblem& pb);
 int wgrad3_run(const GemmProblem& pb, void* ws, size_t ws_bytes, cudaStream_t st);
+// the stem's wgrad over its x4 space-to-depth copy: f32 partials [splits][k][r2*64]
+int wgrad_halo_x4(const void* x4, const void* dy, int n, int p, int q, int k, int r2,
+                  float* partial, int max_splits, int* splits, cudaStream_t st);
 // out[m*ldc + n] = q(prev + sum_s partial[s][m][n]) in fixed split order (gemm_tc.cu)
 int tc_splitk_reduce(int M, int N, int splits, const float* partial, __half* out, int64_t ldc,
                      int acc, int32_t* nonfinite, cudaStream_t st);

@@ -2164,8 +2164,12 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
                           !pb.bnx && pl.splits == 1 &&
                           (int64_t)pl.num_kb * pl.bn * BK * 2 <= RES_MAX);
   }
-  if (pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad))
-    pl.ws_partial = (size_t)pl.splits * pl.M * pl.N * 4;
+  if (pl.splits > 1 || ((pl.c4 || pl.s2d) && pb.mode == kWgrad)) {
+    // the stem's halo wgrad (gemm_wgrad3.cu) splits its pixel tiles over every SM
+    const int sp = (pl.s2d4 && pb.mode == kWgrad && pl.splits < num_sms()) ? num_sms()
+                                                                            : pl.splits;
+    pl.ws_partial = (size_t)sp * pl.M * pl.N * 4;
+  }
   pl.ok = pl.M > 0 && pl.N > 0 && pl.K > 0;
   return pl;
 }
@@ -2582,10 +2586,26 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     if (pb.acc && (rc = map(&tc, pb.out))) return rc;
     args.tma_store = 0;
   }
-  if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, tc, em, args, st);
-  else if (pl.bn == 128) rc = dispatch_bn<128>(pl, ta, tb, tc, em, args, st);
-  else rc = dispatch_bn<256>(pl, ta, tb, tc, em, args, st);
-  if (rc) return rc;
+  // the stem's weight gradient: halo tiles over x4 (gemm_wgrad3.cu) -- one x4
+  // box per 8 x 8 pixel tile for all r2 taps instead of an im2col load per tap
+  bool done = false;
+  if (pl.s2d4 && pb.mode == kWgrad && to_partial && partial) {
+    int used = 0;
+    const int max_sp = (int)(pl.ws_partial / ((size_t)pl.M * pl.N * 4));
+    rc = wgrad_halo_x4(pl.sp_a, pb.a, g.n, g.p, g.q, g.k, pl.g2.r, partial, max_sp, &used, st);
+    if (rc == NNL_OK) {
+      pl.splits = used;
+      done = true;
+    } else if (rc != NNL_ERR_UNSUPPORTED) {
+      return rc;
+    }
+  }
+  if (!done) {
+    if (pl.bn == 64) rc = dispatch_bn<64>(pl, ta, tb, tc, em, args, st);
+    else if (pl.bn == 128) rc = dispatch_bn<128>(pl, ta, tb, tc, em, args, st);
+    else rc = dispatch_bn<256>(pl, ta, tb, tc, em, args, st);
+    if (rc) return rc;
+  }
   if (to_partial) {
     const bool mapped = (pl.c4 || pl.s2d) && pb.mode == kWgrad;
     const int c4 = mapped ? g.c : 0;

@@ -52,8 +52,15 @@ struct W3Args {
   int cblk, nblk;        // c / 64, k / 64
   int splits, tps;       // pixel-tile splits, tiles per split
   int units;
-  float* partial;        // [splits][k][9c] when splits > 1
-  __half* out;           // dW [k][3][3][c]
+  int ntap;              // filter taps (9 for 3x3; 4 for the stem's 4x1 over x4)
+  uint16_t toff[16];     // tap t's view: toff[t] 128 B rows into the halo
+  int hx, hy;            // halo box origin relative to the tile origin
+  uint32_t halo_bytes;
+  int hbw;               // halo box width (pixels) = its row pitch
+  int64_t ld;            // row length of dW / the partials: ntap * c
+  float* partial;        // [splits][k][ld] when splits > 1 (or force_partial)
+  int force_partial;
+  __half* out;           // dW [k][taps][c]
   int acc;
   int32_t* nonfinite;
   int dbg;               // probes (NNL_WG3_DBG): 1 = no MMAs, 2 = no operand loads
@@ -116,12 +123,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&full[s]);
             continue;
           }
-          mbar_arrive_tx(&full[s], kHaloBytes + kDyBytes);
+          mbar_arrive_tx(&full[s], a.halo_bytes + kDyBytes);
           const int img = t / per_img, r = t - img * per_img;
           const int ty = r / a.tw, tx = r - ty * a.tw;
           uint8_t* st = smem + s * kStageBytes;
-          // (10 x 10) halo of 64 channels; out-of-image pixels read as zero (the padding)
-          tma_load_4d(st, &tmX, &full[s], cb * 64, tx * 8 - 1, ty * 8 - 1, img);
+          // the tile's input halo, 64 channels; out-of-image pixels read as zero
+          // (the padding)
+          tma_load_4d(st, &tmX, &full[s], cb * 64, tx * 8 + a.hx, ty * 8 + a.hy, img);
           // (8 x 8) dy tile; pixels past the image edge read as zero (no contribution)
           tma_load_4d(st + kHaloStage, &tmDy, &full[s], nb * 64, tx * 8, ty * 8, img);
         }
@@ -134,16 +142,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the bottleneck: ~10 integer ops per descriptor against a 48-cycle MMA);
     // stage s adds s * kStageBytes / 16 to the start-address field (< 2^14)
     const uint32_t base0 = smem_u32(smem);
+    const int nmt = (a.ntap + 1) / 2;
+    const uint32_t pitch = a.hbw;  // halo row pitch in pixels = the box width
     uint64_t dA[kMT][4], dB[4];
 #pragma unroll
     for (int j = 0; j < kMT; ++j) {
-      const int ta = 2 * j, tb = 2 * j + 1 < 9 ? 2 * j + 1 : 2 * j;
-      const uint32_t oa = (uint32_t)(((ta / 3) * kPitch + ta % 3) * 128);
-      const uint32_t ob = (uint32_t)(((tb / 3) * kPitch + tb % 3) * 128);
+      const int ta = min(2 * j, a.ntap - 1), tb = 2 * j + 1 < a.ntap ? 2 * j + 1 : ta;
+      const uint32_t oa = (uint32_t)a.toff[ta] * 128, ob = (uint32_t)a.toff[tb] * 128;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)  // 16 pixels = tile rows 2kk, 2kk + 1
-        dA[j][kk] = sdesc_sw128(base0 + oa + (uint32_t)(kk * 2 * kPitch * 128), ob - oa,
-                                kPitch * 128);
+        dA[j][kk] = sdesc_sw128(base0 + oa + kk * 2 * pitch * 128, ob - oa, pitch * 128);
     }
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
@@ -165,11 +173,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t so = (uint64_t)((uint32_t)(s * kStageBytes) >> 4);
           const uint32_t acc0 = t > t0 ? 1u : 0u;
 #pragma unroll
-          for (int j = 0; j < kMT; ++j)
+          for (int j = 0; j < kMT; ++j) {
+            if (j >= nmt) break;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               mma_f16(tmem + (uint32_t)(j * 64), dA[j][kk] + so, dB[kk] + so, IDESC,
                       kk ? 1u : acc0);
+          }
           mma_commit(&empty[s]);
         }
         __syncwarp();
@@ -180,7 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int wq = warp - 4;  // TMEM lane quadrant
-    const int64_t ld = 9LL * a.c;
+    const int64_t ld = a.ld;
+    const int nmt = (a.ntap + 1) / 2;
+    const bool to_partial = a.splits > 1 || a.force_partial;
     int ut = 0;
     int bad = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++ut) {
@@ -191,15 +203,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = wq * 32 + lane;  // M row of each tap-pair tile
       const int c = cb * 64 + (row & 63);
 #pragma unroll 1
-      for (int j = 0; j < kMT; ++j) {
+      for (int j = 0; j < nmt; ++j) {
         const int tap = 2 * j + (row >> 6);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t v[32];
           tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(j * 64 + h * 32), v);
-          if (tap >= 9) continue;
+          if (tap >= a.ntap) continue;
           const int n0 = nb * 64 + h * 32;
-          if (a.splits > 1) {
+          if (to_partial) {
             float* p = a.partial + ((int64_t)sp * a.k + n0) * ld + (int64_t)tap * a.c + c;
 #pragma unroll
             for (int e = 0; e < 32; ++e) p[e * ld] = __uint_as_float(v[e]);
@@ -325,6 +337,30 @@ bool wgrad3_eligible(const GemmProblem& pb, int dtype) {
   return dtype == NNL_F16 && w3_enabled() && plan_w3(pb).ok;
 }
 
+static int launch_w3(const CUtensorMap& tx, const CUtensorMap& tdy, const W3Args& a,
+                     cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    NNL_CUDA(cudaFuncSetAttribute(k_tc_wgrad3, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  const int grid = a.units < sm_count() ? a.units : sm_count();
+  launch_k(k_tc_wgrad3, dim3((unsigned)grid), dim3(kThreads), (size_t)kSmem, st, tx, tdy, a);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
+static W3Args base_args(const W3Plan& p, int c, int k) {
+  W3Args a = {};
+  a.c = c; a.k = k;
+  a.tw = p.tw; a.th = p.th; a.tiles = p.tiles;
+  a.cblk = p.cblk; a.nblk = p.nblk;
+  a.splits = p.splits; a.tps = p.tps; a.units = p.units;
+  static const int dbg = getenv("NNL_WG3_DBG") ? atoi(getenv("NNL_WG3_DBG")) : 0;
+  a.dbg = dbg;
+  return a;
+}
+
 int wgrad3_run(const GemmProblem& pb, void* ws, size_t ws_bytes, cudaStream_t st) {
   W3Plan p = plan_w3(pb);
   if (!p.ok) return NNL_ERR_UNSUPPORTED;
@@ -336,11 +372,13 @@ int wgrad3_run(const GemmProblem& pb, void* ws, size_t ws_bytes, cudaStream_t st
   int rc = tmap_nhwc(&tx, pb.b, g.c, g.w, g.h, g.n, kPitch, 10);
   if (rc) return rc;
   if ((rc = tmap_nhwc(&tdy, pb.a, g.k, g.q, g.p, g.n, 8, 8))) return rc;
-  W3Args a;
-  a.c = g.c; a.k = g.k;
-  a.tw = p.tw; a.th = p.th; a.tiles = p.tiles;
-  a.cblk = p.cblk; a.nblk = p.nblk;
-  a.splits = p.splits; a.tps = p.tps; a.units = p.units;
+  W3Args a = base_args(p, g.c, g.k);
+  a.ntap = 9;
+  for (int t = 0; t < 9; ++t) a.toff[t] = (uint16_t)((t / 3) * kPitch + t % 3);
+  a.hx = -1; a.hy = -1;  // pad 1
+  a.hbw = kPitch;
+  a.halo_bytes = kHaloBytes;
+  a.ld = 9LL * g.c;
   float* partial = nullptr;
   if (p.splits > 1)
     partial = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
@@ -348,20 +386,57 @@ int wgrad3_run(const GemmProblem& pb, void* ws, size_t ws_bytes, cudaStream_t st
   a.out = reinterpret_cast<__half*>(pb.out);
   a.acc = pb.acc;
   a.nonfinite = p.splits > 1 ? nullptr : pb.nonfinite;
-  static const int dbg = getenv("NNL_WG3_DBG") ? atoi(getenv("NNL_WG3_DBG")) : 0;
-  a.dbg = dbg;
-  static bool attr = false;
-  if (!attr) {
-    NNL_CUDA(cudaFuncSetAttribute(k_tc_wgrad3, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    attr = true;
-  }
-  const int grid = p.units < sm_count() ? p.units : sm_count();
-  launch_k(k_tc_wgrad3, dim3((unsigned)grid), dim3(kThreads), (size_t)kSmem, st, tx, tdy, a);
-  NNL_CHECK_LAUNCH();
+  if ((rc = launch_w3(tx, tdy, a, st))) return rc;
   if (p.splits > 1)
     return tc_splitk_reduce(g.k, 9 * g.c, p.splits, partial, reinterpret_cast<__half*>(pb.out),
                             9LL * g.c, pb.acc, pb.nonfinite, st);
   return NNL_OK;
+}
+
+// The stem's weight gradient over its space-to-depth copy x4[n][p + r2 - 1][q][64]
+// (gemm_tc.cu s2d_layout: an r2 x 1 convolution over 64 channels): the same
+// halo kernel with r2 vertical taps, halo = 8 x (8 + r2 - 1) x4 pixels (rows
+// 8 pixels apart, so a tap view starts 8 r rows in).  Writes f32 partials
+// [splits][k][r2 * 64] (at most max_splits) for the caller's column-mapping
+// reduction; returns the split count used in *splits.
+int wgrad_halo_x4(const void* x4, const void* dy, int n, int p, int q, int k, int r2,
+                  float* partial, int max_splits, int* splits, cudaStream_t st) {
+  if (!w3_enabled() || q % 8 || k % 64 || r2 < 1 || r2 > 6 || max_splits < 1 ||
+      (reinterpret_cast<uintptr_t>(x4) & 15) || (reinterpret_cast<uintptr_t>(dy) & 15))
+    return NNL_ERR_UNSUPPORTED;
+  W3Plan pl;
+  pl.tw = q / 8;
+  pl.th = (p + 7) / 8;
+  pl.tiles = n * pl.tw * pl.th;
+  pl.cblk = 1;
+  pl.nblk = k / 64;
+  int sp = sm_count() / pl.nblk;
+  if (sp > pl.tiles / 8) sp = pl.tiles / 8;
+  if (sp > max_splits) sp = max_splits;
+  if (sp < 1) sp = 1;
+  pl.tps = (pl.tiles + sp - 1) / sp;
+  pl.splits = (pl.tiles + pl.tps - 1) / pl.tps;
+  pl.units = pl.nblk * pl.splits;
+  pl.ok = true;
+  CUtensorMap tx, tdy;
+  memset(&tx, 0, sizeof(tx));
+  memset(&tdy, 0, sizeof(tdy));
+  int rc = tmap_nhwc(&tx, x4, 64, q, p + r2 - 1, n, 8, 8 + r2 - 1);
+  if (rc) return rc;
+  if ((rc = tmap_nhwc(&tdy, dy, k, q, p, n, 8, 8))) return rc;
+  W3Args a = base_args(pl, 64, k);
+  a.ntap = r2;
+  for (int t = 0; t < r2; ++t) a.toff[t] = (uint16_t)(t * 8);
+  a.hx = 0; a.hy = 0;  // x4 rows are already shifted by the padding
+  a.hbw = 8;
+  a.halo_bytes = (uint32_t)(8 * (8 + r2 - 1) * 128);
+  a.ld = (int64_t)r2 * 64;
+  a.partial = partial;
+  a.force_partial = 1;
+  a.out = nullptr;
+  a.nonfinite = nullptr;
+  *splits = pl.splits;
+  return launch_w3(tx, tdy, a, st);
 }
 
 }  // namespace nnl
