@@ -1401,22 +1401,43 @@ __global__ void k_s2d4(int nimg, int h, int w, int c, int ph, int pw, int hb, in
 
 // k_s2d4 with the two input rows of a block row staged in shared memory
 // (coalesced loads; one CTA per (image, block row)); 16 B stores
+// RY x4 rows per CTA (2 RY input rows staged in shared memory, 16 B loads when
+// the input rows are 16 B multiples), so each CTA's load latency is amortised
+// over RY output rows
 template <int C>
 __global__ void __launch_bounds__(256) k_s2d4_rows(int h, int w, int ph, int pw, int hb, int q,
                                                    const __half* __restrict__ x,
                                                    uint4* __restrict__ x4) {
+  constexpr int RY = 4;
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __half srow[];
-  const int Y = blockIdx.x % hb, n = blockIdx.x / hb;
+  extern __shared__ __half srow_all[];
+  const int groups = (hb + RY - 1) / RY;
+  const int Y0 = (blockIdx.x % groups) * RY, n = blockIdx.x / groups;
   const int rowh = w * C;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < 2 * rowh; i += blockDim.x) {
-    const int r = i >= rowh, j = i - r * rowh;
-    const int ih = 2 * Y + r - ph;
-    srow[i] = (unsigned)ih < (unsigned)h ? x[((int64_t)n * h + ih) * rowh + j] : __float2half(0.f);
+  const int ny = min(RY, hb - Y0);
+  if ((rowh & 7) == 0) {
+    const int row8 = rowh >> 3;
+    uint4* s8 = reinterpret_cast<uint4*>(srow_all);
+    for (int i = threadIdx.x; i < 2 * ny * row8; i += blockDim.x) {
+      const int r = i / row8, j = i - r * row8;
+      const int ih = 2 * Y0 + r - ph;
+      s8[i] = (unsigned)ih < (unsigned)h
+                  ? reinterpret_cast<const uint4*>(x + ((int64_t)n * h + ih) * rowh)[j]
+                  : make_uint4(0u, 0u, 0u, 0u);
+    }
+  } else {
+    for (int i = threadIdx.x; i < 2 * ny * rowh; i += blockDim.x) {
+      const int r = i / rowh, j = i - r * rowh;
+      const int ih = 2 * Y0 + r - ph;
+      srow_all[i] = (unsigned)ih < (unsigned)h ? x[((int64_t)n * h + ih) * rowh + j]
+                                               : __float2half(0.f);
+    }
   }
   __syncthreads();
+  for (int yy = 0; yy < ny; ++yy) {
+  const __half* srow = srow_all + 2 * yy * rowh;
+  const int Y = Y0 + yy;
   uint4* dst = x4 + ((int64_t)n * hb + Y) * q * 8;
   for (int i = threadIdx.x; i < q * 8; i += blockDim.x) {
     const int chunk = i & 7, qq = i >> 3;
@@ -1445,6 +1466,7 @@ __global__ void __launch_bounds__(256) k_s2d4_rows(int h, int w, int ph, int pw,
       }
     }
     dst[i] = *reinterpret_cast<const uint4*>(v);
+  }
   }
 }
 
@@ -2418,10 +2440,10 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
     else last_prep = PrepKey{};
     const int64_t pix = (int64_t)g.n * pl.g2.h * pl.g2.w;
     if (pix >= (1ll << 31)) return fail(NNL_ERR_UNSUPPORTED, "space-to-depth input too large");
-    const bool rows = pl.s2d4 && g.w * g.c * 4 <= 48 * 1024;
+    const bool rows = pl.s2d4 && g.w * g.c * 16 <= 48 * 1024;  // 4 rows x 2 input rows
 #define NNL_S2D4_ROWS(CC)                                                                  \
     if (rows && g.c == CC)                                                                 \
-      launch_k(k_s2d4_rows<CC>, g.n * pl.g2.h, 256, g.w * g.c * 4, st,                           \
+      launch_k(k_s2d4_rows<CC>, g.n * ((pl.g2.h + 3) / 4), 256, g.w * g.c * 16, st,            \
           g.h, g.w, g.ph, g.pw, pl.g2.h, pl.g2.w, src, reinterpret_cast<uint4*>(xs));
     NNL_S2D4_ROWS(1) else NNL_S2D4_ROWS(2) else NNL_S2D4_ROWS(3) else NNL_S2D4_ROWS(4)
     else if (pl.s2d4)

@@ -54,6 +54,8 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--cudnn", action="store_true")
+    ap.add_argument("--stats", action="store_true",
+                    help="forward with the BN-statistics epilogue (as in the training step)")
     ap.add_argument("--once", action="store_true", help="one call per pass (for ncu)")
     ap.add_argument("--ab-pairs", action="store_true",
                     help="also time each pass with CTA pairs disabled (same process)")
@@ -88,8 +90,15 @@ def main():
         flops = 2.0 * b * oh * oh * k * c * r * r
         for ps in passes:
             if ps == "fwd":
+                sp, sh = None, None
+                if args.stats:
+                    rows = int(_lib.lib().nnl_conv2d_stat_rows(C.byref(cs), 1))
+                    if rows > 0:
+                        parts = torch.empty(rows * 2 * k, device=dev)
+                        shift = torch.zeros(k, device=dev)
+                        sp, sh = parts.data_ptr(), shift.data_ptr()
                 fn = lambda: _lib.call("nnl_conv2d_fwd", C.byref(cs), 1, x.data_ptr(), w.data_ptr(),
-                                       bias.data_ptr(), y.data_ptr(), None, None, ws.data_ptr(),
+                                       bias.data_ptr(), y.data_ptr(), sp, sh, ws.data_ptr(),
                                        ws.numel(), st)
                 byts = 2.0 * (x.numel() + w.numel() + y.numel())
             elif ps == "dgrad":
