@@ -156,12 +156,15 @@ def test_bn_large_offset_channels_variance(nnl, half):
 
 
 @pytest.mark.parametrize("offset", [0.0, 64.0])
-def test_conv_epilogue_statistics_are_centred(nnl, offset):
+def test_conv_epilogue_statistics_are_centred(nnl, offset, monkeypatch):
     """Convolution -> BN with the statistics taken in the convolution's
     epilogue (second and later forwards; the first centres its own pass): an
     identity 1x1 convolution reproduces x exactly, so the BN output must match
-    the two-pass reference on channels offset by `offset`, for fresh batches."""
+    the two-pass reference on channels offset by `offset`, for fresh batches.
+    (A 64 -> 64 1x1 convolution takes the streaming statistics pass by default,
+    Convolution.epilogue_stats; NNL_EPI_STATS=1 forces the epilogue.)"""
     import paper_2102_06725_b200.functions as F
+    monkeypatch.setenv("NNL_EPI_STATS", "1")
     _ctx(nnl, True)
     shape = (32, 64, 28, 28)
     c = shape[1]
