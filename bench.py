@@ -100,15 +100,20 @@ def parse():
 
 
 def gemm_traffic() -> dict | None:
-    """DRAM bytes of one step's tcgen05 GEMM launches from the committed ncu
-    capture (profiles/r01_traffic.json, tools/traffic_summary.py)."""
+    """DRAM bytes of one step's tcgen05 GEMM launches (the implicit-GEMM kernel
+    and the halo weight-gradient kernel) from the committed ncu capture
+    (profiles/r02/traffic.json, tools/traffic_summary.py)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            k = json.load(f)["kernels"]["nnl::k_tc_gemm"]
+        with open(os.path.join(ROOT, "profiles", "r02", "traffic.json")) as f:
+            ks = json.load(f)["kernels"]
     except (OSError, KeyError, ValueError):
         return None
-    return {"bytes_per_step": k["dram_bytes_per_launch"] * k["launches"],
-            "launches": k["launches"], "source": "profiles/r01_traffic.json (ncu dram__bytes)"}
+    fams = [k for k in ("nnl::k_tc_gemm", "nnl::k_tc_wgrad3") if k in ks]
+    if not fams:
+        return None
+    return {"bytes_per_step": sum(ks[k]["dram_bytes_per_launch"] * ks[k]["launches"] for k in fams),
+            "launches": sum(ks[k]["launches"] for k in fams), "kernels": fams,
+            "source": "profiles/r02/traffic.json (ncu dram__bytes, one step)"}
 
 
 def peaks() -> dict:

@@ -74,6 +74,8 @@ __device__ __forceinline__ void decode(const W3Args& a, int u, int& cb, int& nb,
   sp = t / a.nblk;
 }
 
+}  // namespace
+
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_wgrad3(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDy,
                 const W3Args a) {
@@ -241,6 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_dealloc(tmem, kTmemCols);
   }
 }
+
+namespace {
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

@@ -39,7 +39,7 @@ def main():
     for d in step:
         if "nnl::" not in d["name"]:
             continue  # e.g. bench.py's GPU-lead spins around profiled nodes
-        k = re.sub(r"\(.*", "", d["name"]).replace("void ", "")
+        k = re.sub(r"\(.*", "", d["name"]).replace("void ", "").replace("<unnamed>::", "")
         k = re.sub(r"<.*", "", k)
         f = fam[k]
         f["launches"] += 1
