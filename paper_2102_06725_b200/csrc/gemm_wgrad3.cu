@@ -39,8 +39,8 @@ constexpr int kPitch = 10;                       // halo row pitch (pixels)
 constexpr int kHaloBytes = kPitch * 10 * 128;    // 12800
 constexpr int kHaloStage = 13312;                // 1024-aligned
 constexpr int kDyBytes = 64 * 128;               // 8 x 8 pixels x 64 channels
-constexpr int kStageBytes = kHaloStage + kDyBytes;
-constexpr int kStages = 8;
+constexpr int kStageBytes = kHaloStage + 2 * kDyBytes;  // room for 128 output channels
+constexpr int kStages = 6;
 constexpr int kMT = 5;                           // tap-pair M tiles
 constexpr int kTmemCols = 512;                   // 5 x 64 used
 constexpr int kThreads = 256;
@@ -53,6 +53,8 @@ struct W3Args {
   int splits, tps;       // pixel-tile splits, tiles per split
   int units;
   int ntap;              // filter taps (9 for 3x3; 4 for the stem's 4x1 over x4)
+  int ngroups;           // tap-pair M tiles split into groups (one pass each): NB = 128
+  uint8_t mt0[3], mt1[3];  // group g covers tap-pair M tiles [mt0[g], mt1[g])
   uint16_t toff[16];     // tap t's view: toff[t] 128 B rows into the halo
   int hx, hy;            // halo box origin relative to the tile origin
   uint32_t halo_bytes;
@@ -66,8 +68,11 @@ struct W3Args {
   int dbg;               // probes (NNL_WG3_DBG): 1 = no MMAs, 2 = no operand loads
 };
 
-__device__ __forceinline__ void decode(const W3Args& a, int u, int& cb, int& nb, int& sp) {
+__device__ __forceinline__ void decode(const W3Args& a, int u, int& cb, int& nb, int& sp,
+                                       int& grp) {
   // consecutive units share the pixel tiles (L2 reuse of x halos and dy tiles)
+  grp = u % a.ngroups;
+  u /= a.ngroups;
   cb = u % a.cblk;
   const int t = u / a.cblk;
   nb = t % a.nblk;
@@ -76,6 +81,9 @@ __device__ __forceinline__ void decode(const W3Args& a, int u, int& cb, int& nb,
 
 }  // namespace
 
+// NB output channels per unit (64, or 128 with the tap pairs split into two
+// passes so that the accumulators fit the 512 TMEM columns)
+template <int NB>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_wgrad3(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDy,
                 const W3Args a) {
@@ -115,8 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-        int cb, nb, sp;
-        decode(a, u, cb, nb, sp);
+        int cb, nb, sp, grp;
+        decode(a, u, cb, nb, sp, grp);
         const int t0 = sp * a.tps, t1 = min(t0 + a.tps, a.tiles);
         for (int t = t0; t < t1; ++t, ++it) {
           const int s = it % kStages;
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&full[s]);
             continue;
           }
-          mbar_arrive_tx(&full[s], a.halo_bytes + kDyBytes);
+          mbar_arrive_tx(&full[s], a.halo_bytes + (NB / 64) * kDyBytes);
           const int img = t / per_img, r = t - img * per_img;
           const int ty = r / a.tw, tx = r - ty * a.tw;
           uint8_t* st = smem + s * kStageBytes;
@@ -133,18 +141,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           // (the padding)
           tma_load_4d(st, &tmX, &full[s], cb * 64, tx * 8 + a.hx, ty * 8 + a.hy, img);
           // (8 x 8) dy tile; pixels past the image edge read as zero (no contribution)
-          tma_load_4d(st + kHaloStage, &tmDy, &full[s], nb * 64, tx * 8, ty * 8, img);
+#pragma unroll
+          for (int h = 0; h < NB / 64; ++h)
+            tma_load_4d(st + kHaloStage + h * kDyBytes, &tmDy, &full[s], nb * NB + 64 * h, tx * 8,
+                        ty * 8, img);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t IDESC = idesc_f16(64, true, true, 128);
+    constexpr uint32_t IDESC = idesc_f16(NB, true, true, 128);
     // all 24 descriptors of stage 0 built once (the issuing thread is otherwise
     // the bottleneck: ~10 integer ops per descriptor against a 48-cycle MMA);
     // stage s adds s * kStageBytes / 16 to the start-address field (< 2^14)
     const uint32_t base0 = smem_u32(smem);
-    const int nmt = (a.ntap + 1) / 2;
     const uint32_t pitch = a.hbw;  // halo row pitch in pixels = the box width
     uint64_t dA[kMT][4], dB[4];
 #pragma unroll
@@ -156,12 +166,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         dA[j][kk] = sdesc_sw128(base0 + oa + kk * 2 * pitch * 128, ob - oa, pitch * 128);
     }
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-      dB[kk] = sdesc_sw128(base0 + kHaloStage + (uint32_t)(kk * 2048), 8192, 1024);
+    for (int kk = 0; kk < 4; ++kk)  // MN-major dy tile: 64-channel chunks kDyBytes apart
+      dB[kk] = sdesc_sw128(base0 + kHaloStage + (uint32_t)(kk * 2048), kDyBytes, 1024);
     int it = 0, ut = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++ut) {
-      int cb, nb, sp;
-      decode(a, u, cb, nb, sp);
+      int cb, nb, sp, grp;
+      decode(a, u, cb, nb, sp, grp);
+      const int jlo = a.mt0[grp], jhi = a.mt1[grp];
       const int t0 = sp * a.tps, t1 = min(t0 + a.tps, a.tiles);
       mbar_wait(tempty, (ut & 1) ^ 1);
       tc_fence_after();
@@ -176,10 +187,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t acc0 = t > t0 ? 1u : 0u;
 #pragma unroll
           for (int j = 0; j < kMT; ++j) {
-            if (j >= nmt) break;
+            if (j < jlo || j >= jhi) continue;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_f16(tmem + (uint32_t)(j * 64), dA[j][kk] + so, dB[kk] + so, IDESC,
+              mma_f16(tmem + (uint32_t)((j - jlo) * NB), dA[j][kk] + so, dB[kk] + so, IDESC,
                       kk ? 1u : acc0);
           }
           mma_commit(&empty[s]);
@@ -193,26 +204,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue
     const int wq = warp - 4;  // TMEM lane quadrant
     const int64_t ld = a.ld;
-    const int nmt = (a.ntap + 1) / 2;
     const bool to_partial = a.splits > 1 || a.force_partial;
     int ut = 0;
     int bad = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++ut) {
-      int cb, nb, sp;
-      decode(a, u, cb, nb, sp);
+      int cb, nb, sp, grp;
+      decode(a, u, cb, nb, sp, grp);
       mbar_wait(tfull, ut & 1);
       tc_fence_after();
       const int row = wq * 32 + lane;  // M row of each tap-pair tile
       const int c = cb * 64 + (row & 63);
 #pragma unroll 1
-      for (int j = 0; j < nmt; ++j) {
+      for (int j = a.mt0[grp]; j < a.mt1[grp]; ++j) {
         const int tap = 2 * j + (row >> 6);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NB / 32; ++h) {
           uint32_t v[32];
-          tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(j * 64 + h * 32), v);
+          tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) +
+                        (uint32_t)((j - a.mt0[grp]) * NB + h * 32), v);
           if (tap >= a.ntap) continue;
-          const int n0 = nb * 64 + h * 32;
+          const int n0 = nb * NB + h * 32;
           if (to_partial) {
             float* p = a.partial + ((int64_t)sp * a.k + n0) * ld + (int64_t)tap * a.c + c;
 #pragma unroll
@@ -287,7 +298,18 @@ int sm_count() {
 struct W3Plan {
   bool ok = false;
   int tw, th, tiles, cblk, nblk, splits, tps, units;
+  int nb = 64, ngroups = 1;  // output block width; tap-pair groups (passes)
 };
+
+// NNL_WG3_NB=64 keeps 64-wide output blocks for every layer (probes)
+int w3_nb128() {
+  static int e = -1;
+  if (e < 0) {
+    const char* s = getenv("NNL_WG3_NB");
+    e = (s && atoi(s) == 64) ? 0 : 1;
+  }
+  return e;
+}
 
 W3Plan plan_w3(const GemmProblem& pb) {
   W3Plan p;
@@ -298,15 +320,24 @@ W3Plan plan_w3(const GemmProblem& pb) {
     return p;
   // 8 x 8 tiles over a 7 x 7 map carry 30 % padding (and the halo 2x the input
   // pixels): the per-tap im2col path is as fast there (measured at 512 ch)
-  if (g.h < 14 || g.w < 14) return p;
+  static const int min_hw = getenv("NNL_WG3_MINHW") ? atoi(getenv("NNL_WG3_MINHW")) : 14;
+  if (g.h < min_hw || g.w < min_hw) return p;
   if ((reinterpret_cast<uintptr_t>(pb.a) & 15) || (reinterpret_cast<uintptr_t>(pb.b) & 15))
     return p;
   p.tw = (g.w + 7) / 8;
   p.th = (g.h + 7) / 8;
   p.tiles = g.n * p.tw * p.th;
   p.cblk = g.c / 64;
-  p.nblk = g.k / 64;
-  const int pairs = p.cblk * p.nblk, sms = sm_count();
+  // 128 output channels per unit when they exist: the N = 128 MMA does twice
+  // the work of N = 64 in 64 instead of 48 cycles (tools/mma_probe.cu); the
+  // nine taps' 128-wide accumulators need two passes (tap pairs 0-2, 3-4) to
+  // fit the 512 TMEM columns
+  if (g.k % 128 == 0 && w3_nb128()) {
+    p.nb = 128;
+    p.ngroups = 2;
+  }
+  p.nblk = g.k / p.nb;
+  const int pairs = p.ngroups * p.cblk * p.nblk, sms = sm_count();
   // one unit per CTA where the (channel block, output block) pairs leave room:
   // splits of the pixel tiles up to the SM count, at least 8 tiles each
   int splits = pairs >= sms ? 1 : sms / pairs;
@@ -341,17 +372,24 @@ bool wgrad3_eligible(const GemmProblem& pb, int dtype) {
   return dtype == NNL_F16 && w3_enabled() && plan_w3(pb).ok;
 }
 
-static int launch_w3(const CUtensorMap& tx, const CUtensorMap& tdy, const W3Args& a,
-                     cudaStream_t st) {
+template <int NB>
+static int launch_w3_nb(const CUtensorMap& tx, const CUtensorMap& tdy, const W3Args& a,
+                        cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    NNL_CUDA(cudaFuncSetAttribute(k_tc_wgrad3, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    NNL_CUDA(cudaFuncSetAttribute(k_tc_wgrad3<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmem));
     attr = true;
   }
   const int grid = a.units < sm_count() ? a.units : sm_count();
-  launch_k(k_tc_wgrad3, dim3((unsigned)grid), dim3(kThreads), (size_t)kSmem, st, tx, tdy, a);
+  launch_k(k_tc_wgrad3<NB>, dim3((unsigned)grid), dim3(kThreads), (size_t)kSmem, st, tx, tdy, a);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
+}
+
+static int launch_w3(const CUtensorMap& tx, const CUtensorMap& tdy, const W3Args& a, int nb,
+                     cudaStream_t st) {
+  return nb == 128 ? launch_w3_nb<128>(tx, tdy, a, st) : launch_w3_nb<64>(tx, tdy, a, st);
 }
 
 static W3Args base_args(const W3Plan& p, int c, int k) {
@@ -360,6 +398,14 @@ static W3Args base_args(const W3Plan& p, int c, int k) {
   a.tw = p.tw; a.th = p.th; a.tiles = p.tiles;
   a.cblk = p.cblk; a.nblk = p.nblk;
   a.splits = p.splits; a.tps = p.tps; a.units = p.units;
+  a.ngroups = p.ngroups;
+  const int mt = kMT;  // tap-pair M tiles of a 3x3 filter (set per caller below)
+  if (p.ngroups == 2) {
+    a.mt0[0] = 0; a.mt1[0] = 3;
+    a.mt0[1] = 3; a.mt1[1] = (uint8_t)mt;
+  } else {
+    a.mt0[0] = 0; a.mt1[0] = (uint8_t)mt;
+  }
   static const int dbg = getenv("NNL_WG3_DBG") ? atoi(getenv("NNL_WG3_DBG")) : 0;
   a.dbg = dbg;
   return a;
@@ -390,7 +436,7 @@ int wgrad3_run(const GemmProblem& pb, void* ws, size_t ws_bytes, cudaStream_t st
   a.out = reinterpret_cast<__half*>(pb.out);
   a.acc = pb.acc;
   a.nonfinite = p.splits > 1 ? nullptr : pb.nonfinite;
-  if ((rc = launch_w3(tx, tdy, a, st))) return rc;
+  if ((rc = launch_w3(tx, tdy, a, p.nb, st))) return rc;
   if (p.splits > 1)
     return tc_splitk_reduce(g.k, 9 * g.c, p.splits, partial, reinterpret_cast<__half*>(pb.out),
                             9LL * g.c, pb.acc, pb.nonfinite, st);
@@ -429,6 +475,7 @@ int wgrad_halo_x4(const void* x4, const void* dy, int n, int p, int q, int k, in
   if (rc) return rc;
   if ((rc = tmap_nhwc(&tdy, dy, k, q, p, n, 8, 8))) return rc;
   W3Args a = base_args(pl, 64, k);
+  a.mt1[0] = (uint8_t)((r2 + 1) / 2);
   a.ntap = r2;
   for (int t = 0; t < r2; ++t) a.toff[t] = (uint16_t)(t * 8);
   a.hx = 0; a.hy = 0;  // x4 rows are already shifted by the padding
@@ -440,7 +487,7 @@ int wgrad_halo_x4(const void* x4, const void* dy, int n, int p, int q, int k, in
   a.out = nullptr;
   a.nonfinite = nullptr;
   *splits = pl.splits;
-  return launch_w3(tx, tdy, a, st);
+  return launch_w3(tx, tdy, a, 64, st);
 }
 
 }  // namespace nnl
