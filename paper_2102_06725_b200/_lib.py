@@ -225,5 +225,61 @@ def workspace(nbytes: int):
     return _ws.buf.data_ptr(), _ws.buf.numel()
 
 
+class _Side(threading.local):
+    """The weight-gradient stream of the engine's backward loop (per thread)."""
+
+    def __init__(self):
+        self.stream = None
+        self.buf = None
+        self.allowed = False
+        self.pending = False
+
+
+_side = _Side()
+
+
+def side_begin(allowed: bool) -> None:
+    """Open a backward pass whose weight gradients may run on the side stream
+    (graph.backward; NNL_WG_STREAM=0 keeps everything on the current stream)."""
+    _side.allowed = bool(allowed) and os.environ.get("NNL_WG_STREAM", "1") != "0"
+    _side.pending = False
+
+
+def side_fork():
+    """Raw handle of the side stream, ordered after everything issued so far on
+    the current stream; None outside an engine backward pass."""
+    if not _side.allowed:
+        return None
+    t = torch()
+    if _side.stream is None:
+        _side.stream = t.cuda.Stream()
+    _side.stream.wait_stream(t.cuda.current_stream())
+    _side.pending = True
+    return _side.stream.cuda_stream
+
+
+def side_end() -> None:
+    """Join the side stream into the current stream (before the optimizer
+    reads the weight gradients) and close the pass."""
+    if _side.pending:
+        torch().cuda.current_stream().wait_stream(_side.stream)
+    _side.pending = False
+    _side.allowed = False
+
+
+def side_workspace(nbytes: int):
+    """The side stream's own scratch buffer (kernels on it run concurrently
+    with the shared workspace's users).  Growth waits for the side stream so
+    the old buffer is idle when it is freed; sizes settle in the first step,
+    before any CUDA-graph capture."""
+    t = torch()
+    nbytes = int(max(nbytes, 1 << 20))
+    if _side.buf is None or _side.buf.numel() < nbytes:
+        if _side.buf is not None and _side.stream is not None:
+            _side.stream.synchronize()
+        _side.buf = t.empty(nbytes + (nbytes >> 2), dtype=t.uint8, device=device())
+    return _side.buf.data_ptr(), _side.buf.numel()
+
+
 def reserve_workspace(nbytes: int) -> None:
     workspace(nbytes)

@@ -306,14 +306,25 @@ class Convolution(FunctionImpl):
         gb = None if node.state.get("bias_by_bn") else gxs[2]
         if gxs[1] is not None or gb is not None:
             own = x.shape[1] <= 4
-            ws = self._workspace(node, cs, x.code, 2)
+            # inside the engine's backward loop the weight gradient runs on the
+            # side stream: nothing later in backward reads dW, and its inputs
+            # (x, dy) are final, so it overlaps the rest of the backward chain
+            # (graph.backward joins before the optimizer)
+            st = _lib.side_fork()
+            if st is not None and not own:
+                ws = _lib.side_workspace(
+                    _lib.lib().nnl_conv2d_workspace_size(C.byref(cs), x.code, 2))
+            else:
+                ws = self._workspace(node, cs, x.code, 2)
+            if st is None:
+                st = _st()
             if own:
                 _lib.lib().nnl_conv2d_prep_reuse(1)
             try:
                 _lib.call("nnl_conv2d_bwd_weight", C.byref(cs), x.code, x.ptr, gy.ptr,
                           gxs[1].ptr if gxs[1] is not None else None, _flag(acc[1]),
                           gb.ptr if gb is not None else None, _flag(acc[2]),
-                          node.state.get("nonfinite_ptr"), ws[0], ws[1], _st())
+                          node.state.get("nonfinite_ptr"), ws[0], ws[1], st)
             finally:
                 if own:
                     _lib.lib().nnl_conv2d_prep_reuse(0)
