@@ -8,6 +8,7 @@ library is missing, or no CUDA device is visible, using the package raises.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
@@ -217,12 +218,63 @@ def workspace(nbytes: int):
 
     Grows monotonically; returns (pointer, size).  Callers never hold it
     across an API call, so reuse by the next kernel on the same stream is safe.
+    Inside `branch_scope()` the branch stream's own buffer is returned.
     """
+    if _branch.active:
+        return _branch_workspace(nbytes)
     t = torch()
     nbytes = int(max(nbytes, 1 << 20))
     if _ws.buf is None or _ws.buf.numel() < nbytes:
         _ws.buf = t.empty(nbytes + (nbytes >> 2), dtype=t.uint8, device=device())
     return _ws.buf.data_ptr(), _ws.buf.numel()
+
+
+class _Branch(threading.local):
+    """A forward branch issued on a second stream (graph.forward)."""
+
+    def __init__(self):
+        self.stream = None
+        self.buf = None
+        self.active = False
+        self.pending = False
+
+
+_branch = _Branch()
+
+
+def _branch_workspace(nbytes: int):
+    t = torch()
+    nbytes = int(max(nbytes, 1 << 20))
+    if _branch.buf is None or _branch.buf.numel() < nbytes:
+        if _branch.buf is not None:
+            _branch.stream.synchronize()  # the old buffer is idle before it is freed
+        _branch.buf = t.empty(nbytes + (nbytes >> 2), dtype=t.uint8, device=device())
+    return _branch.buf.data_ptr(), _branch.buf.numel()
+
+
+@contextlib.contextmanager
+def branch_scope():
+    """Issue the enclosed work on the branch stream, ordered after everything
+    issued so far on the current stream; `branch_join()` later makes the
+    current stream wait for it."""
+    t = torch()
+    cur = t.cuda.current_stream()
+    if _branch.stream is None:
+        _branch.stream = t.cuda.Stream()
+    _branch.stream.wait_stream(cur)
+    _branch.active = True
+    try:
+        with t.cuda.stream(_branch.stream):
+            yield
+    finally:
+        _branch.active = False
+        _branch.pending = True
+
+
+def branch_join() -> None:
+    if _branch.pending:
+        torch().cuda.current_stream().wait_stream(_branch.stream)
+        _branch.pending = False
 
 
 class _Side(threading.local):
