@@ -310,6 +310,16 @@ def side_fork():
     return _side.stream.cuda_stream
 
 
+def wait_aux(stream) -> None:
+    """Make `stream` wait for the side (weight-gradient) and branch streams
+    where they have pending work: a gradient bucket issued on the
+    communication stream may hold gradients either produced."""
+    if _side.pending and _side.stream is not None:
+        stream.wait_stream(_side.stream)
+    if _branch.pending and _branch.stream is not None:
+        stream.wait_stream(_branch.stream)
+
+
 def side_end() -> None:
     """Join the side stream into the current stream (before the optimizer
     reads the weight gradients) and close the pass."""

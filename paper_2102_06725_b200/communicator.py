@@ -468,6 +468,7 @@ class BucketedAllReduce:
         t = _lib.torch()
         plan = self.plans[b]
         self.stream.wait_stream(t.cuda.current_stream())
+        _lib.wait_aux(self.stream)  # gradients from the side / branch streams
         with t.cuda.stream(self.stream):
             self.comm.exchange(plan, True, self.nonfinite_ptr, _lib.stream())
 
