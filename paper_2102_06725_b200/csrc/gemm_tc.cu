@@ -1946,6 +1946,13 @@ static void s2d_layout(const ConvGeom& g, Plan& pl) {
   pl.gh = g.p; pl.gw = g.q; pl.ish = 1; pl.isw = 1; pl.ilh = 0; pl.ilw = 0;
 }
 
+// NNL_WG_MAXGRID caps the persistent grid of weight-gradient GEMMs (probes of
+// the side-stream overlap: fewer SMs for the off-critical-path wgrads)
+static int wg_max_grid() {
+  static const int v = getenv("NNL_WG_MAXGRID") ? atoi(getenv("NNL_WG_MAXGRID")) : 0;
+  return v;
+}
+
 static Plan make_plan(const GemmProblem& pb, int cls = 0) {
   Plan pl;
   const ConvGeom& g = pb.g;
@@ -2193,6 +2200,7 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
                                                                             : pl.splits;
     pl.ws_partial = (size_t)sp * pl.M * pl.N * 4;
   }
+  if (pb.mode == kWgrad && wg_max_grid() > 0) pl.max_grid = wg_max_grid();
   pl.ok = pl.M > 0 && pl.N > 0 && pl.K > 0;
   return pl;
 }

@@ -381,7 +381,9 @@ static int launch_w3_nb(const CUtensorMap& tx, const CUtensorMap& tdy, const W3A
                                   kSmem));
     attr = true;
   }
-  const int grid = a.units < sm_count() ? a.units : sm_count();
+  static const int cap = getenv("NNL_WG_MAXGRID") ? atoi(getenv("NNL_WG_MAXGRID")) : 0;
+  int grid = a.units < sm_count() ? a.units : sm_count();
+  if (cap > 0 && grid > cap) grid = cap;
   launch_k(k_tc_wgrad3<NB>, dim3((unsigned)grid), dim3(kThreads), (size_t)kSmem, st, tx, tdy, a);
   NNL_CHECK_LAUNCH();
   return NNL_OK;
