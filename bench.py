@@ -450,6 +450,9 @@ def main():
     traffic = gemm_traffic() if name == "resnet50" else None
     achieved = gemm_fl / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    # the same GEMM node time against each pass's own roofline min(tensor, AI x HBM)
+    # (the 1x1 layers are HBM-bound, so the tensor fraction alone understates them)
+    layer_bound_ms = PROFILER.gemm_bound_ms(pk.get("bf16_tflops", peak), pk.get("hbm_gbs", 6541.5))
 
     if rank != 0:
         if dist is not None:
@@ -491,6 +494,9 @@ def main():
                      "traffic": (traffic or {}).get("bytes_per_step"), "traffic_detail": traffic,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "gemm_share_of_step": round(gemm_ms / total_ms, 3) if total_ms else None,
+                     "gemm_ms": round(gemm_ms, 3),
+                     "per_pass_bound_ms": round(layer_bound_ms, 3),
+                     "frac_of_per_pass_bound": round(layer_bound_ms / gemm_ms, 4) if gemm_ms else None,
                      "gemm_tflop_per_step": round(gemm_fl / 1e12, 4)},
         "clocks": clk.summary(),
         "last_loss": loss,

@@ -18,10 +18,16 @@ class _Profiler:
     def __init__(self):
         self.enabled = False
         self.gpu_lead_cycles = 0  # > 0: spin the GPU this long before each region
-        self.records = []  # (kind, phase, flops, bytes, start_event, end_event)
+        self.records = []  # (kind, phase, flops, start_event, end_event, description)
+        self.nodes = []    # (node, phase) of each record
 
     def reset(self):
         self.records = []
+        self.nodes = []
+
+    def gemm_bound_ms(self, tflops: float, hbm_gbs: float) -> float:
+        """Sum of the per-pass roofline bounds of the recorded GEMM nodes."""
+        return 1e3 * sum(gemm_bound_s(nd, ph, tflops, hbm_gbs) for nd, ph in self.nodes)
 
     @contextlib.contextmanager
     def region(self, node, phase: str):
@@ -39,6 +45,7 @@ class _Profiler:
         yield
         e.record()
         self.records.append((node.kind, phase, gemm_flops(node, phase), s, e, _describe(node)))
+        self.nodes.append((node, phase))
 
     def per_node(self) -> list[dict]:
         """One entry per recorded node call, in launch order."""
@@ -67,6 +74,35 @@ def _describe(node) -> str:
         s = node.impl.stride[0]
         return f"{ins} -> {o} k{kh} s{s}"
     return ins
+
+
+def gemm_bound_s(node, phase: str, tflops: float, hbm_gbs: float) -> float:
+    """Per-pass roofline bound of a node's implicit GEMMs: for each GEMM the
+    node runs in `phase`, max(FLOPs / tensor peak, bytes / HBM) with every
+    operand and the output moved once in the storage dtype (the per-layer
+    bound of tools/conv_bench.py)."""
+    if node.kind not in ("Convolution", "Affine"):
+        return 0.0
+    es = 2 if node.outputs[0].dtype.value == "f16" else 4
+
+    def n(shape):
+        k = 1
+        for d in shape:
+            k *= d
+        return k
+    x, w, y = n(node.inputs[0].shape), n(node.inputs[1].shape), n(node.outputs[0].shape)
+    one = gemm_flops(node, "fwd")
+
+    def bound(bytes_):
+        return max(one / (tflops * 1e12), es * bytes_ / (hbm_gbs * 1e9))
+    if phase == "fwd":
+        return bound(x + w + y)
+    t = 0.0
+    if node.inputs[0].need_grad:
+        t += bound(y + w + x)   # dgrad: dy, W -> dx
+    if node.inputs[1].need_grad:
+        t += bound(x + y + w)   # wgrad: x, dy -> dW
+    return t
 
 
 def gemm_flops(node, phase: str) -> float:
