@@ -38,6 +38,7 @@ CONV = [  # (B, cin, cout, k, stride, pad, hw)
     (2, 512, 512, 3, 1, 1, 7),     # 7x7 maps: the per-tap im2col wgrad
     (2, 16, 16, 5, 1, 0, 12),      # LeNet conv2: dgrad as a forward conv over flipped weights
     (3, 16, 32, 3, 1, 1, 9),       # same, padded
+    (2, 64, 128, 1, 2, 0, 9),      # 1x1 s2 dgrad, odd extent: the zero-fill pass
 ]
 
 
