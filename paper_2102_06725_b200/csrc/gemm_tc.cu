@@ -52,9 +52,9 @@ enum AMode {
 };
 // A_HALO: stride-1 convolutions over 64 channels (one channel block) -- the 3x3
 // pad-1 layers and the stem's 4x1 convolution over x4: the (8 x 16)-pixel M tile's
-// input halo (3x3: 10 x 18 pixels, rows padded to a 16-pixel pitch; stem: 8 x 19)
+// input halo (3x3: 10 x 18 pixels, a 10-pixel row pitch; stem: 8 x 19)
 // is ONE tiled 4D TMA box per tile, and the nine taps are nine descriptor views
-// into it (view (r, s) starts at halo row r*16 + s: SBO 2048 B, no base offset),
+// into it (view (r, s) starts at halo pixel r*10 + s: SBO 1280 B, no base offset),
 // so each input pixel crosses L2 -> SMEM once per tile instead of once per tap.
 enum BMode {
   B_TMA_K = 0, B_TMA_MN = 1, B_GATHER_WGRAD = 2, B_IM2COL = 3, B_GATHER_C4 = 4, B_IM2COL16 = 5,
@@ -76,7 +76,9 @@ constexpr int RES_MAX = 64 * 1024;
 // 6 KB sets of TMA-loaded input tiles (x, gate, prev: 32 rows x 32 columns each)
 template <int BN, int CG = 1, int RB = 0, int EP = 0, int HL = 0>
 struct Cfg {
-  static constexpr int A_BYTES = HL ? 16 * 18 * 128 : BM * BK * 2;
+  // A_HALO: one halo box per stage -- 3x3: 18 rows x 10-pixel pitch, stem: 19 x 8 --
+  // rounded up to the 1 KB swizzle-atom alignment of the next stage
+  static constexpr int A_BYTES = HL ? (18 * 10 * 128 + 1023) / 1024 * 1024 : BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // this CTA's share of B
   static constexpr int STAGE_B = RB ? 0 : B_BYTES;      // B bytes per ring stage
   static constexpr int RES_BYTES = RB ? (HL ? 9 * B_BYTES : RES_MAX) : 0;
@@ -102,6 +104,16 @@ struct Cfg {
 struct EpiMaps {
   CUtensorMap x, g, o;
 };
+
+// n / d for 0 <= n < 2^31 as (umulhi(n, m) + n) >> s (Granlund-Montgomery with a
+// rounded-up multiplier): the per-tile index math of the epilogue and the
+// producers without the ~20-instruction runtime integer division
+struct FDiv {
+  uint32_t m, s;
+};
+__device__ __forceinline__ int fdiv(int n, FDiv d) {
+  return (int)((__umulhi((uint32_t)n, d.m) + (uint32_t)n) >> d.s);
+}
 
 struct TcArgs {
   int64_t K;          // reduction length (B_GATHER_C4: pixels)
@@ -153,14 +165,16 @@ struct TcArgs {
   const float *bn_mean, *bn_istd, *bn_gamma, *bn_beta;
   int bn_relu, bn_canon;
   __half* bn_out;
+  // fast divisors: tiles_m * tiles_n, tiles_n, stw, sth, sbw, sbh, rgw, rgh
+  FDiv fd_pers, fd_tn, fd_stw, fd_sth, fd_sbw, fd_sbh, fd_rgw, fd_rgh;
 };
 
 // origin (x, y, image) of spatial box `tile`
 __device__ __forceinline__ void sp_origin(const TcArgs& a, int tile, int& x0, int& y0, int& n0) {
-  const int xt = tile % a.stw, t2 = tile / a.stw;
-  x0 = xt * a.sbw;
-  y0 = (t2 % a.sth) * a.sbh;
-  n0 = (t2 / a.sth) * a.sbi;
+  const int t2 = fdiv(tile, a.fd_stw), t3 = fdiv(t2, a.fd_sth);
+  x0 = (tile - t2 * a.stw) * a.sbw;
+  y0 = (t2 - t3 * a.sth) * a.sbh;
+  n0 = t3 * a.sbi;
 }
 
 struct Unit {
@@ -170,9 +184,9 @@ struct Unit {
 __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int u) {
   Unit w;
   const int per_split = a.tiles_m * a.tiles_n;
-  w.split = u / per_split;
+  w.split = fdiv(u, a.fd_pers);
   const int rem = u - w.split * per_split;
-  w.tm = rem / a.tiles_n;
+  w.tm = fdiv(rem, a.fd_tn);
   w.tn = rem - w.tm * a.tiles_n;
   w.kb0 = w.split * a.kb_per_split;
   w.nk = min(w.kb0 + a.kb_per_split, a.num_kb) - w.kb0;
@@ -476,8 +490,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       : sdesc_sw128(bbase, 16, 1024);
           if (AM == A_HALO) {
             if (elect_one()) {
-              for (int tp = 0; tp < a.hl_r * a.hl_s; ++tp) {
-                const int r = tp / a.hl_s, sx = tp - a.hl_s * r;
+              for (int r = 0, tp = 0; r < a.hl_r; ++r)
+              for (int sx = 0; sx < a.hl_s; ++sx, ++tp) {
                 // the 128B swizzle follows the absolute shared-memory address (as the
                 // TMA wrote it), so a view starting s rows into a swizzle atom needs
                 // no base offset (measured: base offset s gives wrong products)
@@ -746,17 +760,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ex0 = 0, ey0 = 0, en0 = 0;
       if (kSp) sp_origin(a, m0 / BM, ex0, ey0, en0);
       // A_HALO tiles overhang the grid bottom: rows past the last image row are idle
-      const bool mv = kSp ? (m0 / BM < a.sp_tiles &&
-                             (AM != A_HALO || ey0 + row / a.sbw < a.sgh))
+      // tile row -> (bx, by, bi) of the pixel box (x fastest, then y, then image)
+      const int rq = kSp ? fdiv(row, a.fd_sbw) : 0, rbi = kSp ? fdiv(rq, a.fd_sbh) : 0;
+      const int rbx = row - rq * a.sbw, rby = rq - rbi * a.sbh;
+      const bool mv = kSp ? (m0 / BM < a.sp_tiles && (AM != A_HALO || ey0 + rq < a.sgh))
                           : m < a.M;
       int64_t orow = m;
-      if (kSp) {  // tile row -> output pixel (x fastest, then y, then image)
-        const int bx = row % a.sbw, t2 = row / a.sbw;
-        orow = ((int64_t)(en0 + t2 / a.sbh) * a.sgh + ey0 + t2 % a.sbh) * a.sgw + ex0 + bx;
-      }
+      if (kSp) orow = ((int64_t)(en0 + rbi) * a.sgh + ey0 + rby) * a.sgw + ex0 + rbx;
+      // box coordinates of the warp's first row (its 32 rows are a sub-box)
+      const int wrq = kSp ? fdiv(32 * wq, a.fd_sbw) : 0, wrb = kSp ? fdiv(wrq, a.fd_sbh) : 0;
+      const int wcx = ex0 + 32 * wq - wrq * a.sbw, wcy = ey0 + wrq - wrb * a.sbh, wcn = en0 + wrb;
       if (a.remap && mv) {
-        const int x = m % a.rgw, tt = m / a.rgw;
-        const int y = tt % a.rgh, n = tt / a.rgh;
+        const int tt = fdiv(m, a.fd_rgw), x = m - tt * a.rgw;
+        const int n = fdiv(tt, a.fd_rgh), y = tt - n * a.rgh;
         orow = ((int64_t)n * g.h + y * a.rsh + a.ra) * g.w + x * a.rsw + a.rb;
       }
       // accumulate mode through TMA: the previous values of each 32-column chunk
@@ -771,9 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_read<0>();  // this half's previous store has read it
           mbar_arrive_tx(&ebar[ew * 2 + (k & 1)], 2048);
           if (kSp) {
-            const int rr = 32 * wq, t2 = rr / a.sbw;
-            tma_load_4d(bb, &tmC, &ebar[ew * 2 + (k & 1)], n0 + cc, ex0 + rr % a.sbw,
-                        ey0 + t2 % a.sbh, en0 + t2 / a.sbh);
+            tma_load_4d(bb, &tmC, &ebar[ew * 2 + (k & 1)], n0 + cc, wcx, wcy, wcn);
           } else {
             tma_load_2d(bb, &tmC, &ebar[ew * 2 + (k & 1)], n0 + cc, m0 + 32 * wq);
           }
@@ -789,8 +803,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_read<0>();  // this set's previous store has read it
           mbar_arrive_tx(bar, 2048u * (1u + (a.bn_gate ? 1u : 0u) + (a.acc ? 1u : 0u)));
           if (kSp) {
-            const int rr = 32 * wq, t2 = rr / a.sbw;
-            const int cx = ex0 + rr % a.sbw, cy = ey0 + t2 % a.sbh, cn = en0 + t2 / a.sbh;
+            const int cx = wcx, cy = wcy, cn = wcn;
             tma_load_4d(bb, &em.x, bar, n0 + cc, cx, cy, cn);
             if (a.bn_gate) tma_load_4d(bb + 2048, &em.g, bar, n0 + cc, cx, cy, cn);
             if (a.acc) tma_load_4d(bb + 4096, &tmC, bar, n0 + cc, cx, cy, cn);
@@ -900,9 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if (kSp) {
-              const int rr = 32 * wq, t2 = rr / a.sbw;
-              tma_store_4d(&em.o, bs, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
-                           en0 + t2 / a.sbh);
+              tma_store_4d(&em.o, bs, n0 + c, wcx, wcy, wcn);
             } else {
               tma_store_2d(&em.o, bs, n0 + c, m0 + 32 * wq);
             }
@@ -948,9 +959,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if (kSp) {
-              const int rr = 32 * wq, t2 = rr / a.sbw;
-              tma_store_4d(&tmC, buf, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
-                           en0 + t2 / a.sbh);
+              tma_store_4d(&tmC, buf, n0 + c, wcx, wcy, wcn);
             } else {
               tma_store_2d(&tmC, buf, n0 + c, m0 + 32 * wq);
             }
@@ -1000,9 +1009,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if (kSp) {  // the warp's 32 rows are a sub-box of the pixel box
-              const int rr = 32 * wq, t2 = rr / a.sbw;
-              tma_store_4d(&tmC, buf, n0 + c, ex0 + rr % a.sbw, ey0 + t2 % a.sbh,
-                           en0 + t2 / a.sbh);
+              tma_store_4d(&tmC, buf, n0 + c, wcx, wcy, wcn);
             } else {
               tma_store_2d(&tmC, buf, n0 + c, m0 + 32 * wq);
             }
@@ -1036,24 +1043,54 @@ __global__ void __launch_bounds__(kThreads, 1)
                 rp[2] = s1b;
                 rp[3] = s2b;
               }
-            } else {  // lane owns column c + lane
-              float s1 = 0.f, s2 = 0.f;
-              const float kc = bias_s[BN + c + lane];
-#pragma unroll 8
-              for (int r = 0; r < 32; ++r) {
-                const float x = __half2float(*reinterpret_cast<const __half*>(
-                    buf + r * 64 + (((lane >> 3) ^ ((r >> 1) & 3)) << 4) + (lane & 7) * 2));
-                const float d = (vrows >> r) & 1 ? x - kc : 0.f;
-                s1 += d;
-                s2 += d * d;
+            } else {
+              // lane owns the column pair c + 2p, c + 2p + 1 (p = lane & 15) over
+              // rows 16h .. 16h + 15 (h = lane >> 4), half2 loads; the upper half
+              // walks its rows in (i ^ 1) order so the two halves of the warp read
+              // the two different 64 B bank halves; halves combined by one shuffle
+              const int p = lane & 15, h = lane >> 4;
+              const float ka = bias_s[BN + c + 2 * p], kb = bias_s[BN + c + 2 * p + 1];
+              const uint8_t* bp = buf + (p & 3) * 4;
+              float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
+              if (vrows == 0xffffffffu) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const int r = 16 * h + (i ^ h);
+                  const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
+                      bp + r * 64 + (((p >> 2) ^ ((r >> 1) & 3)) << 4)));
+                  const float da = x.x - ka, db = x.y - kb;
+                  s1a += da;
+                  s1b += db;
+                  s2a += da * da;
+                  s2b += db * db;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const int r = 16 * h + (i ^ h);
+                  const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
+                      bp + r * 64 + (((p >> 2) ^ ((r >> 1) & 3)) << 4)));
+                  const bool ok = (vrows >> r) & 1;
+                  const float da = ok ? x.x - ka : 0.f, db = ok ? x.y - kb : 0.f;
+                  s1a += da;
+                  s1b += db;
+                  s2a += da * da;
+                  s2b += db * db;
+                }
               }
+              s1a += __shfl_xor_sync(0xffffffffu, s1a, 16);
+              s1b += __shfl_xor_sync(0xffffffffu, s1b, 16);
+              s2a += __shfl_xor_sync(0xffffffffu, s2a, 16);
+              s2b += __shfl_xor_sync(0xffffffffu, s2b, 16);
               if (reg_stats) {
                 float* ra = racc[(c - c_lo) / CW];
-                ra[0] += s1; ra[1] += s2;
-              } else {
-                float* rp = red + ((wq * BN) + c + lane) * 2;
-                rp[0] = s1;
-                rp[1] = s2;
+                ra[0] += s1a; ra[1] += s2a; ra[2] += s1b; ra[3] += s2b;
+              } else if (h == 0) {
+                float* rp = red + ((wq * BN) + c + 2 * p) * 2;
+                rp[0] = s1a;
+                rp[1] = s2a;
+                rp[2] = s1b;
+                rp[3] = s2b;
               }
             }
           }
@@ -1184,9 +1221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (CW == 64) {
           float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
           rp[0] = racc[k][0]; rp[1] = racc[k][1]; rp[2] = racc[k][2]; rp[3] = racc[k][3];
-        } else {
-          float* rp = red + ((wq * BN) + c + lane) * 2;
-          rp[0] = racc[k][0]; rp[1] = racc[k][1];
+        } else if (lane < 16) {  // column pair c + 2 lane, c + 2 lane + 1
+          float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
+          rp[0] = racc[k][0]; rp[1] = racc[k][1]; rp[2] = racc[k][2]; rp[3] = racc[k][3];
         }
       }
       named_sync(1, kEpiThreads);
@@ -1746,7 +1783,7 @@ struct Plan {
   int sbw = 0, sbh = 0, sbi = 0, stw = 0, sth = 0, sp_tiles = 0, slw = 0, slh = 0;
   int sgw = 0, sgh = 0;
   bool halo = false;     // A_HALO (see the enum)
-  int hl_pitch = 16, hl_r = 3, hl_s = 3;
+  int hl_pitch = 10, hl_r = 3, hl_s = 3;
   const void* sp_a = nullptr;  // tensor of the A boxes: dims (sp_ac, sgw, sgh, n)
   const void* sp_b = nullptr;  // wgrad B boxes: dims (sp_bc, bw_, bh_, n)
   int sp_ac = 0, sp_bc = 0, sp_bw = 0, sp_bh = 0, sp_n = 0;
@@ -2588,6 +2625,15 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   }
   TcArgs args;
   memset(&args, 0, sizeof(args));
+  auto fd = [](int d) {  // FDiv for 1 <= d < 2^31 (d <= 0: unused, zero)
+    FDiv f = {0u, 0u};
+    if (d <= 0) return f;
+    uint32_t p = 0;
+    while ((1ull << p) < (unsigned long long)d) ++p;
+    f.m = (uint32_t)(((1ull << 32) * ((1ull << p) - (unsigned long long)d)) / (unsigned long long)d + 1);
+    f.s = p;
+    return f;
+  };
   args.M = pl.M; args.N = pl.N; args.num_kb = pl.num_kb; args.kb_per_split = pl.kb_per_split;
   args.tiles_m = pl.tiles_m; args.tiles_n = pl.tiles_n; args.units = pl.units;
   args.g = pl.s2d ? pl.g2 : g;
@@ -2617,6 +2663,10 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   args.sbw = pl.sbw; args.sbh = pl.sbh; args.sbi = pl.sbi; args.stw = pl.stw; args.sth = pl.sth;
   args.sp_tiles = pl.sp_tiles; args.slw = pl.slw; args.slh = pl.slh;
   args.sgw = pl.sgw; args.sgh = pl.sgh;
+  args.fd_pers = fd(pl.tiles_m * pl.tiles_n); args.fd_tn = fd(pl.tiles_n);
+  args.fd_stw = fd(pl.stw); args.fd_sth = fd(pl.sth);
+  args.fd_sbw = fd(pl.sbw); args.fd_sbh = fd(pl.sbh);
+  args.fd_rgw = fd(pl.rgw); args.fd_rgh = fd(pl.rgh);
   args.res_kb = pl.halo ? pl.hl_r * pl.hl_s : 0;
   args.hl_pitch = pl.hl_pitch; args.hl_r = pl.hl_r; args.hl_s = pl.hl_s;
   args.hl_bytes = (uint32_t)(pl.hl_pitch * (pl.sbh + pl.hl_r - 1) * 128);
