@@ -745,6 +745,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = tid; j < BN; j += kEpiThreads) {
           const bool ok = n0 + j < a.N;
           if (a.bias) bias_s[j] = ok ? __half2float(a.bias[n0 + j]) : 0.f;
+          // EP = 0: the bias with -0 made +0 in bias_s[2 BN + j]: q(0 + (acc + b))
+          // == q(acc + (b + 0)) for every acc and b, one add instead of two
+          if (EP == 0 && a.bias) bias_s[2 * BN + j] = __fadd_rn(bias_s[j], 0.f);
           if (EP == 0 && a.stats) bias_s[BN + j] = ok && a.stat_shift ? a.stat_shift[n0 + j] : 0.f;
           if (EP == 1) {
             bias_s[BN + j] = ok ? a.bn_mean[n0 + j] : 0.f;
@@ -989,12 +992,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int k = 8 * j + 2 * e;
-              float f0 = __uint_as_float(v[k]), f1 = __uint_as_float(v[k + 1]);
-              if (a.bias) {
-                f0 = __fadd_rn(f0, bias_s[c + k]);
-                f1 = __fadd_rn(f1, bias_s[c + k + 1]);
-              }
-              const __half2 h = __floats2half2_rn(__fadd_rn(0.f, f0), __fadd_rn(0.f, f1));
+              // packed f32x2 add (FADD2): q(0 + (acc + b)) as q(acc + (b + 0))
+              const float2 f = __fadd2_rn(
+                  make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                  a.bias ? *reinterpret_cast<const float2*>(&bias_s[2 * BN + c + k])
+                         : make_float2(0.f, 0.f));
+              const __half2 h = __floats2half2_rn(f.x, f.y);
               pk[e] = mv ? *reinterpret_cast<const uint32_t*>(&h) : 0u;
             }
             if (a.nonfinite) {
@@ -1019,29 +1022,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             // sums of (y - K) over the warp's VALID rows (idle rows are staged
             // as zeros, which would otherwise count as -K)
             const uint32_t vrows = __ballot_sync(0xffffffffu, mv);
+            // per column pair: s1 += y - K, s2 += (y - K)^2 with packed f32x2
+            // FADD2 / FFMA2 (the same RN ops as the scalar FADD / contracted FFMA)
+            auto acc2 = [](float2& s1, float2& s2, float2 x, float2 nk, bool ok) {
+              float2 d = __fadd2_rn(x, nk);
+              if (!ok) d = make_float2(0.f, 0.f);
+              s1 = __fadd2_rn(s1, d);
+              s2 = __ffma2_rn(d, d, s2);
+            };
             if (CW == 64) {  // lane owns columns c + 2*lane, c + 2*lane + 1
-              float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
-              const float ka = bias_s[BN + c + 2 * lane], kb = bias_s[BN + c + 2 * lane + 1];
+              float2 s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
+              const float2 nk = make_float2(-bias_s[BN + c + 2 * lane],
+                                            -bias_s[BN + c + 2 * lane + 1]);
+              const uint8_t* bp = buf + (lane & 3) * 4;
+              if (vrows == 0xffffffffu) {
 #pragma unroll 8
-              for (int r = 0; r < 32; ++r) {
-                const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
-                    buf + r * 128 + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4));
-                const float da = (vrows >> r) & 1 ? x.x - ka : 0.f;
-                const float db = (vrows >> r) & 1 ? x.y - kb : 0.f;
-                s1a += da;
-                s1b += db;
-                s2a += da * da;
-                s2b += db * db;
+                for (int r = 0; r < 32; ++r)
+                  acc2(s1, s2, __half22float2(*reinterpret_cast<const __half2*>(
+                                   bp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4))), nk, true);
+              } else {
+#pragma unroll 8
+                for (int r = 0; r < 32; ++r)
+                  acc2(s1, s2, __half22float2(*reinterpret_cast<const __half2*>(
+                                   bp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4))), nk,
+                       (vrows >> r) & 1);
               }
               if (reg_stats) {
                 float* ra = racc[(c - c_lo) / CW];
-                ra[0] += s1a; ra[1] += s2a; ra[2] += s1b; ra[3] += s2b;
+                ra[0] += s1.x; ra[1] += s2.x; ra[2] += s1.y; ra[3] += s2.y;
               } else {
                 float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
-                rp[0] = s1a;
-                rp[1] = s2a;
-                rp[2] = s1b;
-                rp[3] = s2b;
+                rp[0] = s1.x;
+                rp[1] = s2.x;
+                rp[2] = s1.y;
+                rp[3] = s2.y;
               }
             } else {
               // lane owns the column pair c + 2p, c + 2p + 1 (p = lane & 15) over
@@ -1049,35 +1063,26 @@ __global__ void __launch_bounds__(kThreads, 1)
               // walks its rows in (i ^ 1) order so the two halves of the warp read
               // the two different 64 B bank halves; halves combined by one shuffle
               const int p = lane & 15, h = lane >> 4;
-              const float ka = bias_s[BN + c + 2 * p], kb = bias_s[BN + c + 2 * p + 1];
+              const float2 nk = make_float2(-bias_s[BN + c + 2 * p], -bias_s[BN + c + 2 * p + 1]);
               const uint8_t* bp = buf + (p & 3) * 4;
-              float s1a = 0.f, s1b = 0.f, s2a = 0.f, s2b = 0.f;
+              float2 s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
               if (vrows == 0xffffffffu) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                   const int r = 16 * h + (i ^ h);
-                  const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
-                      bp + r * 64 + (((p >> 2) ^ ((r >> 1) & 3)) << 4)));
-                  const float da = x.x - ka, db = x.y - kb;
-                  s1a += da;
-                  s1b += db;
-                  s2a += da * da;
-                  s2b += db * db;
+                  acc2(s1, s2, __half22float2(*reinterpret_cast<const __half2*>(
+                                   bp + r * 64 + (((p >> 2) ^ ((r >> 1) & 3)) << 4))), nk, true);
                 }
-              } else {
+              } else if (vrows) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                   const int r = 16 * h + (i ^ h);
-                  const float2 x = __half22float2(*reinterpret_cast<const __half2*>(
-                      bp + r * 64 + (((p >> 2) ^ ((r >> 1) & 3)) << 4)));
-                  const bool ok = (vrows >> r) & 1;
-                  const float da = ok ? x.x - ka : 0.f, db = ok ? x.y - kb : 0.f;
-                  s1a += da;
-                  s1b += db;
-                  s2a += da * da;
-                  s2b += db * db;
+                  acc2(s1, s2, __half22float2(*reinterpret_cast<const __half2*>(
+                                   bp + r * 64 + (((p >> 2) ^ ((r >> 1) & 3)) << 4))), nk,
+                       (vrows >> r) & 1);
                 }
               }
+              float s1a = s1.x, s1b = s1.y, s2a = s2.x, s2b = s2.y;
               s1a += __shfl_xor_sync(0xffffffffu, s1a, 16);
               s1b += __shfl_xor_sync(0xffffffffu, s1b, 16);
               s2a += __shfl_xor_sync(0xffffffffu, s2a, 16);
