@@ -74,6 +74,11 @@ int nnl_set_tc_tile4(int enabled);
    (8 x 16)-pixel tile (nine descriptor views) instead of one load per tap;
    returns the previous setting, < 0 only queries (default 1; env NNL_HALO=0) */
 int nnl_set_tc_halo(int enabled);
+/* 8-warp GEMM epilogues of single-N-tile, TMA-stored outputs interleaved by
+   tile (warps 4..7 even tiles, 8..11 odd ones, all columns each) instead of
+   split by columns; returns the previous setting, < 0 only queries (default 1;
+   env NNL_EPI_IL=0) */
+int nnl_set_tc_epi_il(int enabled);
 
 /* ---- geometry ----------------------------------------------------------- */
 typedef struct nnl_conv_shape {

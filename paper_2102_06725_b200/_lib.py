@@ -82,6 +82,7 @@ _SIGS = {
     "nnl_set_tc_s2d4": (C.c_int, [C.c_int]),
     "nnl_set_tc_tile4": (C.c_int, [C.c_int]),
     "nnl_set_tc_halo": (C.c_int, [C.c_int]),
+    "nnl_set_tc_epi_il": (C.c_int, [C.c_int]),
     "nnl_conv2d_prep_reuse": (C.c_int, [C.c_int]),
     "nnl_quantize_f16": (C.c_int, [i64, p, p, p]),
     "nnl_fill": (C.c_int, [C.c_int, i64, p, f32, p]),

@@ -418,6 +418,17 @@ int nnl_set_tc_halo(int enabled) {
   if (enabled >= 0) v = enabled ? 1 : 0;
   return prev;
 }
+
+int nnl_set_tc_epi_il(int enabled) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NNL_EPI_IL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  const int prev = v;
+  if (enabled >= 0) v = enabled ? 1 : 0;
+  return prev;
+}
 int nnl_set_tc_s2d4(int enabled) {
   static int v = -1;
   if (v < 0) {

@@ -167,6 +167,7 @@ struct TcArgs {
   __half* bn_out;
   // fast divisors: tiles_m * tiles_n, tiles_n, stw, sth, sbw, sbh, rgw, rgh
   FDiv fd_pers, fd_tn, fd_stw, fd_sth, fd_sbw, fd_sbh, fd_rgw, fd_rgh;
+  int epi_il;         // allow tile-interleaved 8-warp epilogues (see k_tc_gemm)
 };
 
 // origin (x, y, image) of spatial box `tile`
@@ -245,6 +246,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TMA-store chunk width: 64 columns (128 B rows, 128 B swizzle), or 32 (64 B
   // rows, 64 B swizzle) when eight warps share a 64-wide tile
   constexpr int CW = (kEpi8 && BN == 64) ? 32 : 64;
+  // tile-interleaved 8-warp epilogue (single N tile, plain TMA-store outputs):
+  // warps 4..7 take the even tiles (accumulator buffer 0) and warps 8..11 the
+  // odd ones (buffer 1), each warp all BN columns of its 32 rows -- two tiles'
+  // epilogues overlap per SM sub-partition and the per-tile index / barrier /
+  // store-issue work is paid by four warps instead of eight
+  const bool il = kEpi8 && EP == 0 && a.epi_il && a.tiles_n == 1 && a.tma_store && !a.acc;
 
   extern __shared__ uint8_t smem_raw[];
   // offset from the shared array itself (not via an integer cast), so that
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpi * CG);
+      mbar_init(&tempty[b], (il ? 4 : kEpi) * CG);
     }
     mbar_init(bfull, 1);
     for (int b = 0; b < 16; ++b) mbar_init(&ebar[b], 1);
@@ -714,8 +721,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // [BN/2, BN) (two warps per SM sub-partition hide each other's latency)
     const int ew = warp - kEpiWarp0;         // epilogue warp 0 .. kEpi - 1
     const int wq = warp & 3;                 // TMEM lane quarter
-    const int c_lo = kEpi8 ? (ew >> 2) * (BN / 2) : 0;
-    const int c_hi = kEpi8 ? c_lo + BN / 2 : BN;
+    const int grp = ew >> 2;                 // kEpi8: warp group 0 / 1
+    const int c_lo = kEpi8 && !il ? grp * (BN / 2) : 0;
+    const int c_hi = kEpi8 && !il ? c_lo + BN / 2 : BN;
     constexpr int kEpiThreads = 32 * kEpi;
     const int tid = threadIdx.x - 32 * kEpiWarp0;
     if (a.stats) {
@@ -733,7 +741,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     float racc[4][4] = {};
     // the leader's tempty barriers (the MMA waits on both CTAs' epilogues)
     const uint32_t te0 = CG == 2 ? mapa_shared(&tempty[0], 0) : smem_u32(&tempty[0]);
+    if (il && (a.bias || a.stats)) {  // one N tile: its bias / centre slices once
+      staged_n0 = 0;
+      named_sync(2, kEpiThreads);
+      for (int j = tid; j < BN; j += kEpiThreads) {
+        const bool ok = j < a.N;
+        if (a.bias) bias_s[j] = ok ? __half2float(a.bias[j]) : 0.f;
+        if (a.bias) bias_s[2 * BN + j] = __fadd_rn(bias_s[j], 0.f);
+        if (a.stats) bias_s[BN + j] = ok && a.stat_shift ? a.stat_shift[j] : 0.f;
+      }
+      named_sync(2, kEpiThreads);
+    }
     for (int u = pair; u < a.units; u += npairs, ++t) {
+      if (il && (t & 1) != grp) continue;
       const Unit w = decode_unit(a, u);
       const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN;
       const int ab = t & 1;
@@ -1221,28 +1241,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (reg_stats) {  // combine the row-quarter warps: red[q][col] -> stat_s[col]
-      for (int k = 0; k * CW < c_hi - c_lo; ++k) {
-        const int c = c_lo + k * CW;
-        if (CW == 64) {
-          float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
-          rp[0] = racc[k][0]; rp[1] = racc[k][1]; rp[2] = racc[k][2]; rp[3] = racc[k][3];
-        } else if (lane < 16) {  // column pair c + 2 lane, c + 2 lane + 1
-          float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
-          rp[0] = racc[k][0]; rp[1] = racc[k][1]; rp[2] = racc[k][2]; rp[3] = racc[k][3];
-        }
-      }
-      named_sync(1, kEpiThreads);
-      for (int col = tid; col < BN && col < a.N; col += kEpiThreads) {
-        float t1 = 0.f, t2 = 0.f;
+      // (tile-interleaved: group 0's quarters, then group 1's added -- fixed order)
+      for (int pass = 0; pass < (il ? 2 : 1); ++pass) {
+        if (!il || grp == pass)
+          for (int k = 0; k * CW < c_hi - c_lo; ++k) {
+            const int c = c_lo + k * CW;
+            if (CW == 64) {
+              float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
+              rp[0] = racc[k][0]; rp[1] = racc[k][1]; rp[2] = racc[k][2]; rp[3] = racc[k][3];
+            } else if (lane < 16) {  // column pair c + 2 lane, c + 2 lane + 1
+              float* rp = red + ((wq * BN) + c + 2 * lane) * 2;
+              rp[0] = racc[k][0]; rp[1] = racc[k][1]; rp[2] = racc[k][2]; rp[3] = racc[k][3];
+            }
+          }
+        named_sync(1, kEpiThreads);
+        for (int col = tid; col < BN && col < a.N; col += kEpiThreads) {
+          float t1 = 0.f, t2 = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          t1 += red[(q * BN + col) * 2 + 0];
-          t2 += red[(q * BN + col) * 2 + 1];
+          for (int q = 0; q < 4; ++q) {
+            t1 += red[(q * BN + col) * 2 + 0];
+            t2 += red[(q * BN + col) * 2 + 1];
+          }
+          stat_s[col] = pass ? stat_s[col] + t1 : t1;
+          stat_s[C::MAX_STAT_N + col] = pass ? stat_s[C::MAX_STAT_N + col] + t2 : t2;
         }
-        stat_s[col] = t1;
-        stat_s[C::MAX_STAT_N + col] = t2;
+        named_sync(1, kEpiThreads);
       }
-      named_sync(1, kEpiThreads);
     }
     if (a.stats) {  // one partial row per CTA: stats[blockIdx.x][2][N]
       for (int col = tid; col < a.N; col += kEpiThreads) {
@@ -1815,6 +1839,8 @@ static bool halo_layout(const ConvGeom& g, int cin, int w, int h, const void* sr
   pl.M = pl.sp_tiles * BM;
   return true;
 }
+// tile-interleaved 8-warp epilogues (env NNL_EPI_IL=0: column-split epilogues)
+static int epi_il_env() { return nnl_set_tc_epi_il(-1); }
 // accumulate-mode outputs through TMA load/store (env NNL_TMA_ACC=0: direct stores)
 static bool use_tma_acc_env() {
   static int v = -1;
@@ -2672,6 +2698,7 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
   args.fd_stw = fd(pl.stw); args.fd_sth = fd(pl.sth);
   args.fd_sbw = fd(pl.sbw); args.fd_sbh = fd(pl.sbh);
   args.fd_rgw = fd(pl.rgw); args.fd_rgh = fd(pl.rgh);
+  args.epi_il = epi_il_env();
   args.res_kb = pl.halo ? pl.hl_r * pl.hl_s : 0;
   args.hl_pitch = pl.hl_pitch; args.hl_r = pl.hl_r; args.hl_s = pl.hl_s;
   args.hl_bytes = (uint32_t)(pl.hl_pitch * (pl.sbh + pl.hl_r - 1) * 128);

@@ -419,3 +419,49 @@ def test_halo_tiles_match_per_tap_loads(nnl, geom):
             _lib.lib().nnl_set_tc_halo(prev)
     for a, c in zip(outs[0], outs[1]):
         assert _rel_err(a, c) < 2e-3
+
+
+@pytest.mark.parametrize("geom", [(4, 64, 64, 3, 1, 1, 56), (2, 3, 64, 7, 2, 3, 64),
+                                  (4, 64, 256, 1, 1, 0, 28), (3, 128, 128, 1, 1, 0, 20),
+                                  (2, 256, 64, 1, 1, 0, 17)])
+def test_interleaved_epilogue_matches_column_split(nnl, geom):
+    """Tile-interleaved 8-warp epilogues (warp groups on alternate tiles, all
+    columns each) against the column-split epilogue: identical output bits
+    (bias with a -0 entry: q(0 + (acc + b)) == q(acc + (b + 0))), and BN
+    statistics equal up to the association of the per-CTA f32 sums."""
+    import torch
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    b, cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (cout, cin, k, k)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, (cout,)).astype(np.float32)
+    bias[0] = -0.0
+    shift = torch.from_numpy(rng.uniform(-0.2, 0.2, cout).astype(np.float32)).cuda()
+
+    class _Bn:
+        state = {"shift_ready": True, "shift": shift}
+    outs = []
+    for mode in (1, 0):
+        prev = _lib.lib().nnl_set_tc_epi_il(mode)
+        try:
+            vs = [nnl.Variable(a.shape) for a in (x, w, bias)]
+            for v, a in zip(vs, (x, w, bias)):
+                v.d = a
+            y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+            node = y.parent
+            node.state["emit_stats"] = True
+            node.state["stat_bn"] = _Bn
+            node.impl.forward(node, [v.data for v in vs], [y.data])
+            y.data.mark_set()
+            rows = node.state["stat_rows"]
+            st = node.state["stats"].cpu().numpy()[: rows * 2 * cout]
+            outs.append((y.d.copy(), st.reshape(rows, 2, cout).astype(np.float64).sum(0)))
+        finally:
+            _lib.lib().nnl_set_tc_epi_il(prev)
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-5, atol=1e-4)
+    ov = [O.Var(a, half=True) for a in (x, w, bias)]
+    assert _rel_err(outs[0][0], O.conv2d(*ov, (s, s), (p, p), True).value) < 4e-3
