@@ -1055,11 +1055,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float2 nk = make_float2(-bias_s[BN + c + 2 * lane],
                                             -bias_s[BN + c + 2 * lane + 1]);
               const uint8_t* bp = buf + (lane & 3) * 4;
-              if (vrows == 0xffffffffu) {
-#pragma unroll 8
-                for (int r = 0; r < 32; ++r)
+              if (vrows == 0xffffffffu) {  // two accumulator chains (even / odd rows)
+                float2 t1 = make_float2(0.f, 0.f), t2 = make_float2(0.f, 0.f);
+#pragma unroll 16
+                for (int r = 0; r < 32; r += 2) {
                   acc2(s1, s2, __half22float2(*reinterpret_cast<const __half2*>(
                                    bp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4))), nk, true);
+                  acc2(t1, t2, __half22float2(*reinterpret_cast<const __half2*>(
+                                   bp + (r + 1) * 128 + (((lane >> 2) ^ ((r + 1) & 7)) << 4))),
+                       nk, true);
+                }
+                s1 = __fadd2_rn(s1, t1);
+                s2 = __fadd2_rn(s2, t2);
               } else {
 #pragma unroll 8
                 for (int r = 0; r < 32; ++r)
@@ -1086,13 +1093,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float2 nk = make_float2(-bias_s[BN + c + 2 * p], -bias_s[BN + c + 2 * p + 1]);
               const uint8_t* bp = buf + (p & 3) * 4;
               float2 s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
-              if (vrows == 0xffffffffu) {
+              if (vrows == 0xffffffffu) {  // two accumulator chains (even / odd i)
+                float2 t1 = make_float2(0.f, 0.f), t2 = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  const int r = 16 * h + (i ^ h);
+                for (int i = 0; i < 16; i += 2) {
+                  const int r = 16 * h + (i ^ h), r1 = 16 * h + ((i + 1) ^ h);
                   acc2(s1, s2, __half22float2(*reinterpret_cast<const __half2*>(
                                    bp + r * 64 + (((p >> 2) ^ ((r >> 1) & 3)) << 4))), nk, true);
+                  acc2(t1, t2, __half22float2(*reinterpret_cast<const __half2*>(
+                                   bp + r1 * 64 + (((p >> 2) ^ ((r1 >> 1) & 3)) << 4))), nk, true);
                 }
+                s1 = __fadd2_rn(s1, t1);
+                s2 = __fadd2_rn(s2, t2);
               } else if (vrows) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
