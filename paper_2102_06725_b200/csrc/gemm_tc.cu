@@ -393,7 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             load4d(stA + s * C::A_BYTES, &tmA, 0, a_x + a.slw, a_y + a.slh, a_n);
           } else if (AM == A_TILE4) {
             const int t = kb / a.cblk, cb = kb - t * a.cblk;
-            const int r = t / g.s, sx = t - r * g.s;
+            int r, sx;  // strided-dgrad class: the tap's dy offsets from the table
+            if (a.ntap) { r = a.tap_offh[t]; sx = a.tap_offw[t]; }
+            else { r = t / g.s; sx = t - r * g.s; }
             load4d(stA + s * C::A_BYTES, &tmA, cb * 64, a_x + sx + a.slw, a_y + r + a.slh, a_n);
           } else if (AM == A_TILE4MN) {
 #pragma unroll
@@ -1821,6 +1823,8 @@ struct Plan {
   int s2 = 0;            // block-tap columns per block row of the column order
   // spatial tiles (A_TILE4 / A_TILE4MN / B_TILE4), see TcArgs
   bool sp = false;
+  bool sp_cls = false;   // strided-dgrad class over spatial tiles: 4D store into the
+                         // class's strided view of dx (pixel (ra, rb) + (rsh, rsw) steps)
   int sbw = 0, sbh = 0, sbi = 0, stw = 0, sth = 0, sp_tiles = 0, slw = 0, slh = 0;
   int sgw = 0, sgh = 0;
   bool halo = false;     // A_HALO (see the enum)
@@ -1886,13 +1890,16 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // tiled 4D view of an NHWC fp16 tensor (dims C, W, H, N innermost first)
 static int make_tmap4(CUtensorMap* tm, const void* ptr, int c, int w, int h, int n,
-                      const int box[4], CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                      const int box[4], CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                      const int64_t* bstrides = nullptr) {  // byte strides of w, h, n
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(NNL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (c * 2) % 16)
     return fail(NNL_ERR_UNSUPPORTED, "TMA 4D operand not 16-byte aligned");
   cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
   cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  if (bstrides)
+    for (int i = 0; i < 3; ++i) strides[i] = (cuuint64_t)bstrides[i];
   cuuint32_t bx[4] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2],
                       (cuuint32_t)box[3]};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -2135,9 +2142,23 @@ static Plan make_plan(const GemmProblem& pb, int cls = 0) {
       pl.nclass = g.sh * g.sw;
       pl.M = (int)((int64_t)g.n * pl.gh * pl.gw);
       pl.K = pl.ntap * g.k;
-      pl.amode = A_IM2COL; pl.cblk = g.k / 64;
-      pl.im = {pb.a, g.k, g.q, g.p, g.n, pl.ilw, pl.ilh, pl.gw - g.q + pl.ilw,
-               pl.gh - g.p + pl.ilh, 1, 1, BM};
+      pl.cblk = g.k / 64;
+      // spatial tiles over the class grid (one tiled 4D dy box per tap, stored
+      // through the class's strided 4D view of dx) when a pixel box tiles it and
+      // the classes tile dx exactly; else TMA im2col rows + row-remapped stores
+      if (use_tile4() && g.h == pl.gh * g.sh && g.w == pl.gw * g.sw && use_tma_store() &&
+          (!pb.acc || use_tma_acc_env()) && !(reinterpret_cast<uintptr_t>(pb.out) & 15) &&
+          g.c % 8 == 0 && sp_box(pl.gw, pl.gh, g.n, BM, pl)) {
+        pl.sp = true; pl.sp_cls = true; pl.remap = false;
+        pl.amode = A_TILE4;
+        pl.slw = pl.ilw; pl.slh = pl.ilh; pl.sgw = pl.gw; pl.sgh = pl.gh;
+        pl.sp_a = pb.a; pl.sp_ac = g.k; pl.sp_bw = g.q; pl.sp_bh = g.p; pl.sp_n = g.n;
+        pl.M = pl.sp_tiles * BM;
+      } else {
+        pl.amode = A_IM2COL;
+        pl.im = {pb.a, g.k, g.q, g.p, g.n, pl.ilw, pl.ilh, pl.gw - g.q + pl.ilw,
+                 pl.gh - g.p + pl.ilh, 1, 1, BM};
+      }
     } else if (!pb.bnx && halo_layout(g, g.k, g.w, g.h, pb.a, g.c, pl)) {
       pl.flip = 1;  // dgrad: tap t uses weight tap 8 - t (resident B)
     } else if (g.sh == 1 && g.sw == 1 && use_tile4() && sp_box(g.w, g.h, g.n, BM, pl)) {
@@ -2740,12 +2761,22 @@ static int run_plan(const GemmProblem& pb, Plan pl, void* ws, cudaStream_t st) {
       const int bw32 = pl.sbw < 32 ? pl.sbw : 32;
       const int bh32 = pl.sbh < 32 / bw32 ? pl.sbh : 32 / bw32;
       const int box[4] = {cw32 ? 32 : 64, bw32, bh32, 32 / (bw32 * bh32)};
-      if ((rc = make_tmap4(&tc, pb.out, pl.N, pl.sgw, pl.sgh, pl.sp_n, box, sw))) return rc;
+      if (pl.sp_cls) {  // the class pixels (y*rsh + ra, x*rsw + rb) of dx as a 4D view
+        const int64_t W = (int64_t)g.w, H = (int64_t)g.h, row = (int64_t)pl.N * 2;
+        const int64_t bs[3] = {pl.rsw * row, pl.rsh * W * row, H * W * row};
+        const uint8_t* base =
+            reinterpret_cast<const uint8_t*>(pb.out) + ((int64_t)pl.ra * W + pl.rb) * row;
+        if ((rc = make_tmap4(&tc, base, pl.N, pl.sgw, pl.sgh, pl.sp_n, box, sw, bs))) return rc;
+      } else if ((rc = make_tmap4(&tc, pb.out, pl.N, pl.sgw, pl.sgh, pl.sp_n, box, sw))) {
+        return rc;
+      }
     } else if ((rc = make_tmap(&tc, o, cw32 ? 32 : 64, 32, sw))) {
       return rc;
     }
     args.tma_store = 1;
   }
+  if (pl.sp_cls && !args.tma_store)
+    return fail(NNL_ERR_UNSUPPORTED, "strided-dgrad spatial class needs the TMA-store epilogue");
   if (pb.bnx) {  // x / gate / prev / gated-output maps: 32 x 32 boxes, 64 B swizzle
     if ((pl.ldc * 2) % 16) return fail(NNL_ERR_UNSUPPORTED, "fused BN-backward: row stride");
     auto map = [&](CUtensorMap* m, const void* ptr) -> int {

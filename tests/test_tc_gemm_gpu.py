@@ -465,3 +465,38 @@ def test_interleaved_epilogue_matches_column_split(nnl, geom):
     np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-5, atol=1e-4)
     ov = [O.Var(a, half=True) for a in (x, w, bias)]
     assert _rel_err(outs[0][0], O.conv2d(*ov, (s, s), (p, p), True).value) < 4e-3
+
+
+@pytest.mark.parametrize("geom", [(8, 128, 128, 3, 2, 1, 56), (32, 256, 256, 3, 2, 1, 28),
+                                  (16, 64, 128, 3, 2, 1, 32)])
+def test_strided_dgrad_spatial_classes(nnl, geom):
+    """Stride-2 3x3 dgrad parity classes over spatial tiles (one tiled 4D dy box
+    per class tap, TMA-stored through the class's strided 4D view of dx) against
+    the TMA-im2col class GEMMs with row-remapped stores: identical dx bits (same
+    tap and channel-block order), and the oracle's input gradient."""
+    import paper_2102_06725_b200.functions as F
+    from paper_2102_06725_b200 import _lib
+    _half(nnl)
+    b, cin, cout, k, s, p, hw = geom
+    rng = np.random.default_rng(31)
+    x = rng.uniform(-1, 1, (b, cin, hw, hw)).astype(np.float32)
+    w = rng.uniform(-0.1, 0.1, (cout, cin, k, k)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, (cout,)).astype(np.float32)
+    outs = []
+    for mode in (1, 0):
+        prev = _lib.lib().nnl_set_tc_tile4(mode)
+        try:
+            vs = [nnl.Variable(a.shape, need_grad=True) for a in (x, w, bias)]
+            for v, a in zip(vs, (x, w, bias)):
+                v.d = a
+            y = F.convolution(*vs, stride=(s, s), pad=(p, p))
+            y.forward()
+            y.backward(1.0)
+            outs.append(vs[0].g.copy())
+        finally:
+            _lib.lib().nnl_set_tc_tile4(prev)
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    ov = [O.Var(a, half=True, need_grad=True) for a in (x, w, bias)]
+    oy = O.conv2d(*ov, (s, s), (p, p), True)
+    gxs = oy.parent.bwd([np.ones(oy.value.shape, np.float32)], [True, False, False])
+    assert _rel_err(outs[0], O.q16(gxs[0])) < 4e-3
