@@ -179,6 +179,16 @@ int nnl_conv2d_bwd_data_bn(const nnl_conv_shape* cs, int dtype, const void* dy, 
 /* ---- MaxPooling: functions.py:217-291 ----------------------------------- */
 int nnl_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x, void* y,
                     uint8_t* argmax, void* stream);
+/* BatchNormalization (batch statistics already finalised into save_mean /
+   save_istd by nnl_bn_fwd_train with y = NULL) -> ReLU -> max pooling in one
+   pass: y = maxpool(relu(q(gamma * ((x - mean) * istd) + beta))), argmax as
+   nnl_maxpool_fwd; relu(BN(x)) is never written (engine fusion of
+   functions.py:412-416, :307-314 and :217-291; fp16, C % 8 == 0, 3x3 windows
+   with stride 2). */
+int nnl_bn_relu_maxpool_ok(int dtype, const nnl_pool_shape* ps);
+int nnl_bn_relu_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x,
+                            const float* gamma, const float* beta, const float* save_mean,
+                            const float* save_istd, void* y, uint8_t* argmax, void* stream);
 int nnl_maxpool_bwd(int dtype, const nnl_pool_shape* ps, const void* dy,
                     const uint8_t* argmax, void* dx, int accumulate, void* stream);
 
@@ -218,7 +228,9 @@ size_t nnl_bn_workspace_size(int64_t rows, int32_t c);
    feed backward.
    residual (nullable): the residual tail BN -> Add2 -> [ReLU] in one pass,
    y = [relu](q(q(BN(x)) + residual)) -- each step rounded exactly as the
-   separate functions would (functions.py:412-416, then Add2, then ReLU). */
+   separate functions would (functions.py:412-416, then Add2, then ReLU).
+   y = NULL: statistics only (running stats, save_mean / save_istd, shift),
+   for a consumer that applies them itself (nnl_bn_relu_maxpool_fwd). */
 int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x,
                      const float* gamma, const float* beta,
                      float* running_mean, float* running_var, float eps, float momentum,

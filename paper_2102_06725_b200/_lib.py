@@ -104,6 +104,8 @@ _SIGS = {
     "nnl_conv2d_bwd_data_bn": (C.c_int, [p, C.c_int, p, p, p, C.c_int, p, p, sz, p]),
     "nnl_maxpool_fwd": (C.c_int, [C.c_int, p, p, p, p, p]),
     "nnl_maxpool_bwd": (C.c_int, [C.c_int, p, p, p, p, C.c_int, p]),
+    "nnl_bn_relu_maxpool_ok": (C.c_int, [C.c_int, p]),
+    "nnl_bn_relu_maxpool_fwd": (C.c_int, [C.c_int, p, p, p, p, p, p, p, p, p]),
     "nnl_relu_fwd": (C.c_int, [C.c_int, i64, p, p, p]),
     "nnl_relu_bwd": (C.c_int, [C.c_int, i64, p, p, p, C.c_int, p]),
     "nnl_add2_fwd": (C.c_int, [C.c_int, i64, p, p, p, C.c_int, p]),

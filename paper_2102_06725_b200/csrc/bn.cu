@@ -678,6 +678,7 @@ int nnl_bn_fwd_train(int dtype, int64_t rows, int32_t c, const void* x, const fl
       parts, R, c, rows, running_mean, running_var, eps, momentum, save_mean, save_istd,
       stat_partials ? shift : nullptr, stat_partials ? nullptr : x, dtype == NNL_F16, shift);
   NNL_CHECK_LAUNCH();
+  if (!y) return NNL_OK;  // statistics only: the consumer applies them
   return bn_apply_fwd(dtype, rows, c, x, gamma, beta, save_mean, save_istd, y, residual,
                       fuse_relu, st);
 }

@@ -299,6 +299,102 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd_k3s2_rows(nnl_pool_shape ps
   }
 }
 
+// BatchNormalization -> ReLU -> 3x3 / stride-2 max pool in one pass (the ResNet
+// stem; engine fusion, clear_buffer=True): one CTA per (image, output row) stages
+// the three input rows of x = the BN input, applied as the separate BN-apply
+// pass would -- z = q(gamma * ((x - mean) * istd) + beta) with f32 RN steps
+// (functions.py:412-416, bn_stream.cu APPLY_F) in packed f32x2 ops, then
+// ReLU with NaN passing and -0 -> +0 -- and pools z with the same first-max /
+// NaN-wins rule as the plain pool (pool9_k3).  z itself is never written: the
+// pool's backward uses its argmax, BN's backward recomputes the gate from x.
+__global__ void __launch_bounds__(256) k_bn_relu_maxpool_k3s2_rows(
+    nnl_pool_shape ps, const uint4* __restrict__ x, const float* __restrict__ gamma,
+    const float* __restrict__ beta, const float* __restrict__ mean,
+    const float* __restrict__ istd, uint4* __restrict__ y, uint2* __restrict__ arg) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ uint4 rows[];
+  const int cg = ps.c >> 3, rowv = ps.w * cg;
+  // a thread's staged vectors are all of channel group threadIdx.x % cg (cg
+  // divides the block and the row): its eight channels' constants in registers
+  const int c8 = (threadIdx.x % cg) * 8;
+  float2 nm[4], is2[4], ga2[4], be2[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int c = c8 + 2 * e;
+    nm[e] = make_float2(-mean[c], -mean[c + 1]);
+    is2[e] = make_float2(istd[c], istd[c + 1]);
+    ga2[e] = make_float2(gamma[c], gamma[c + 1]);
+    be2[e] = beta ? make_float2(beta[c], beta[c + 1]) : make_float2(0.f, 0.f);
+  }
+  const int op = blockIdx.x % ps.p, b = blockIdx.x / ps.p;
+  const int h0 = op * 2 - ps.ph;
+  // eight 16 B loads in flight per thread before any is used (one memory
+  // latency per batch instead of one per element)
+  constexpr int kB = 8;
+  for (int i0 = threadIdx.x; i0 < 3 * rowv; i0 += kB * blockDim.x) {
+    uint4 vb[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int i = i0 + k * blockDim.x;
+      const int r = i / rowv, j = i - r * rowv;
+      vb[k] = i < 3 * rowv && (unsigned)(h0 + r) < (unsigned)ps.h
+                  ? __ldg(x + (int64_t)(b * ps.h + h0 + r) * rowv + j)
+                  : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+    const int i = i0 + k * blockDim.x;
+    if (i >= 3 * rowv) break;
+    const int r = i / rowv;
+    const int ih = h0 + r;
+    uint4 o = make_uint4(0, 0, 0, 0);
+    if ((unsigned)ih < (unsigned)ps.h) {
+      const uint4 v = vb[k];
+      const uint32_t* vw = reinterpret_cast<const uint32_t*>(&v);
+      uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 xv = __half22float2(*reinterpret_cast<const __half2*>(&vw[e]));
+        const float2 xh = __fmul2_rn(__fadd2_rn(xv, nm[e]), is2[e]);
+        const float2 zf = __fadd2_rn(__fmul2_rn(ga2[e], xh), be2[e]);
+        const __half2 q = __floats2half2_rn(zf.x, zf.y);
+        const uint32_t qw = *reinterpret_cast<const uint32_t*>(&q);
+        // ReLU: keep q > 0 and NaN, everything else (negatives, -0) becomes +0
+        const uint32_t keep = __hgt2_mask(q, __float2half2_rn(0.f)) |
+                              __vcmpgtu2(qw & 0x7fff7fffu, 0x7c007c00u);
+        ow[e] = qw & keep;
+      }
+    }
+    rows[i] = o;
+    }
+  }
+  __syncthreads();
+  constexpr uint32_t kNegInf = 0xfc00fc00u;
+  for (int i = threadIdx.x; i < ps.q * cg; i += blockDim.x) {
+    const int g = i % cg, oq = i / cg;
+    const int w0 = oq * 2 - ps.pw;
+    uint4 u[9];
+#pragma unroll
+    for (int di = 0; di < 3; ++di) {
+      const bool rin = (unsigned)(h0 + di) < (unsigned)ps.h;
+      const uint4* rp = rows + di * rowv + g;
+#pragma unroll
+      for (int dj = 0; dj < 3; ++dj) {
+        const int iw = w0 + dj;
+        u[di * 3 + dj] = rin && (unsigned)iw < (unsigned)ps.w
+                             ? rp[iw * cg] : make_uint4(kNegInf, kNegInf, kNegInf, kNegInf);
+      }
+    }
+    uint4 yo;
+    uint2 a;
+    pool9_k3(u, yo, a);
+    const int64_t oi = ((int64_t)(b * ps.p + op) * ps.q + oq) * cg + g;
+    y[oi] = yo;
+    arg[oi] = a;
+  }
+}
+
 // Backward of the 3x3 / stride 2 / pad 1 pool: one thread per 2x2 input block
 // (2a..2a+1, 2b..2b+1) x 8 channels.  Those four pixels are only reached by
 // outputs (a..a+1, b..b+1): 4 dy + 4 index loads for 4 pixels, summed per
@@ -528,6 +624,31 @@ int nnl_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x, void* y,
   NNL_CHECK_LAUNCH();
   return NNL_OK;
 }
+
+int nnl_bn_relu_maxpool_ok(int dtype, const nnl_pool_shape* ps) {
+  return ps && dtype == NNL_F16 && ps->c % 8 == 0 && ps->kh == 3 && ps->kw == 3 &&
+         ps->sh == 2 && ps->sw == 2 && 3 * ps->w * ps->c * 2 <= 48 * 1024 &&
+         256 % (ps->c / 8) == 0 &&
+         (int64_t)ps->n * ps->h * ps->w * ps->c < (1ll << 31);
+}
+
+int nnl_bn_relu_maxpool_fwd(int dtype, const nnl_pool_shape* ps, const void* x,
+                            const float* gamma, const float* beta, const float* save_mean,
+                            const float* save_istd, void* y, uint8_t* argmax, void* stream) {
+  if (!ps) return fail(NNL_ERR_INVALID_ARGUMENT, "null pool shape");
+  const int rows_bytes = 3 * ps->w * ps->c * 2;
+  if (!nnl_bn_relu_maxpool_ok(dtype, ps))
+    return fail(NNL_ERR_UNSUPPORTED, "fused BN-ReLU-maxpool: fp16, C %% 8 == 0, 3x3 / stride 2");
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+        reinterpret_cast<uintptr_t>(argmax)) & 15) != 0)
+    return fail(NNL_ERR_UNSUPPORTED, "fused BN-ReLU-maxpool: buffers not 16 B aligned");
+  if ((int64_t)ps->n * ps->p * ps->q * ps->c <= 0) return NNL_OK;
+  launch_k(k_bn_relu_maxpool_k3s2_rows, ps->n * ps->p, 256, rows_bytes, as_stream(stream),
+           *ps, (const uint4*)x, gamma, beta, save_mean, save_istd, (uint4*)y, (uint2*)argmax);
+  NNL_CHECK_LAUNCH();
+  return NNL_OK;
+}
+
 
 int nnl_maxpool_bwd(int dtype, const nnl_pool_shape* ps, const void* dy, const uint8_t* argmax,
                     void* dx, int accumulate, void* stream) {

@@ -516,7 +516,8 @@ class BatchNormalization(FunctionImpl):
             shift = _state_buf(node, "shift", c)
             _lib.call("nnl_bn_fwd_train", x.code, rows, c, x.ptr, gamma.ptr, beta.ptr, mean.ptr,
                       var.ptr, float(np.float32(self.eps)), float(np.float32(self.momentum)),
-                      parts, nparts, shift.data_ptr(), sm.data_ptr(), si.data_ptr(), y.ptr,
+                      parts, nparts, shift.data_ptr(), sm.data_ptr(), si.data_ptr(),
+                      y.ptr if y is not None else None,
                       residual.ptr if residual is not None else None, 1 if relu else 0,
                       ws[0], ws[1], _st())
             node.state["shift_ready"] = True
@@ -531,6 +532,31 @@ class BatchNormalization(FunctionImpl):
     def forward_fused(self, node, relu_node, stats):
         # backward recomputes the ReLU gate from x, so the output may be released
         self._forward(node, relu_node.outputs[0].data, relu=True)
+
+    def can_fuse_relu_pool(self, node, pool_node) -> bool:
+        """BN -> ReLU -> MaxPooling as one pass (nnl_bn_relu_maxpool_fwd): batch
+        statistics, fp16, and a 3x3 / stride-2 pool the fused kernel covers."""
+        try:
+            x = node.inputs[0].data
+            ps = pool_node.impl._ps(x.shape)
+            return bool(self.batch_stat and node.inputs[0].data.code == _lib.F16
+                        and node.inputs[2].data.code == _lib.F32
+                        and _lib.lib().nnl_bn_relu_maxpool_ok(x.code, C.byref(ps)))
+        except Exception:
+            return False
+
+    def forward_fused_pool(self, node, relu_node, pool_node):
+        # statistics (finalize) only, then BN-apply + ReLU + pool in one pass:
+        # relu(BN(x)) is never written; the pool's backward uses its argmax and
+        # BN's backward recomputes the ReLU gate from x
+        self._forward(node, None, relu=True)
+        x, gamma, beta = (v.data for v in node.inputs[:3])
+        ps = pool_node.impl._ps(x.shape)
+        y = pool_node.outputs[0].data
+        arg = _state_buf(pool_node, "argmax", y.size, _lib.torch().uint8)
+        _lib.call("nnl_bn_relu_maxpool_fwd", x.code, C.byref(ps), x.ptr, gamma.ptr, beta.ptr,
+                  node.state["mean"].data_ptr(), node.state["istd"].data_ptr(), y.ptr,
+                  arg.data_ptr(), _st())
 
     def _backward(self, node, gy: NdArray, fused_relu: bool, gxs, acc, gate=None, dres=None,
                   acc_res=False):

@@ -129,3 +129,48 @@ def test_graph_replay_refuses_bad_labels(nnl, golden):
     with pytest.raises(LabelOutOfRange):
         tr.step_async(g["lenet_x"][0], bad)
     tr.step(g["lenet_x"][0], g["lenet_labels"])  # valid labels replay again
+
+
+def _stem_run(nnl, fuse_pool, monkeypatch):
+    import paper_2102_06725_b200.functions as F
+    import paper_2102_06725_b200.parametric as PF
+    monkeypatch.setenv("NNL_FUSE_POOL", "1" if fuse_pool else "0")
+    nnl.set_default_context(nnl.ExecutionContext(type_config=nnl.TypeConfig.HALF))
+    x = O.uniform(3, 0, (4, 3, 64, 64), -1, 1)
+    lab = (np.arange(4) % 10).astype(np.float32)
+    with nnl.registry_scope(nnl.ParameterRegistry(0)) as reg:
+        xv = nnl.Variable(x.shape)
+        tv = nnl.Variable(lab.shape)
+        h = PF.convolution(xv, 64, (7, 7), stride=(2, 2), pad=(3, 3), name="conv1")
+        z = F.relu(PF.batch_normalization(h, name="bn1"))
+        pool = F.max_pooling(z, (3, 3), (2, 2), pad=(1, 1))
+        h = PF.convolution(pool, 64, (3, 3), pad=(1, 1), name="conv2")
+        h = F.relu(PF.batch_normalization(h, name="bn2"))
+        h = F.global_average_pooling(h)
+        loss = F.softmax_cross_entropy(PF.affine(h, 10, name="fc"), tv)
+        xv.d, tv.d = x, lab
+        loss.forward(clear_buffer=True)
+        pd = pool.d.copy()
+        loss.backward(grad_seed=8.0, clear_buffer=True)
+        out = float(loss.d), pd, {k: v.g.copy() for k, v in reg.get_parameters().items()}
+    nnl.set_default_context(nnl.ExecutionContext())
+    return out
+
+
+def test_bn_relu_maxpool_fusion_is_bit_identical(nnl, monkeypatch):
+    """The stem's BN -> ReLU -> MaxPooling as one pass (opt-in NNL_FUSE_POOL=1;
+    relu(BN(x)) never written, the pool's argmax from the fused kernel): loss,
+    pooled activations and every parameter gradient bit-identical to the
+    BN->ReLU pass + pool."""
+    import paper_2102_06725_b200.functions as F
+    calls = []
+    orig = F.BatchNormalization.forward_fused_pool
+    monkeypatch.setattr(F.BatchNormalization, "forward_fused_pool",
+                        lambda self, *a: (calls.append(1), orig(self, *a))[1])
+    l1, p1, g1 = _stem_run(nnl, True, monkeypatch)
+    assert calls == [1]  # the stem's BN -> ReLU -> pool took the fused pass
+    l0, p0, g0 = _stem_run(nnl, False, monkeypatch)
+    assert l1 == l0
+    assert np.array_equal(p1.view(np.uint32), p0.view(np.uint32))
+    for k in g0:
+        assert np.array_equal(g1[k].view(np.uint32), g0[k].view(np.uint32)), k
