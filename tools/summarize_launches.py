@@ -19,7 +19,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
     ap.add_argument("out")
-    ap.add_argument("--step", type=int, default=-2, help="index among complete steps")
+    ap.add_argument("--step", type=int, default=-4,
+                    help="index among complete steps (bench.py ends with two profiled eager steps)")
     args = ap.parse_args()
     rows = list(csv.reader(open(args.csv)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
